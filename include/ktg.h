@@ -1,0 +1,218 @@
+/*
+ * ktg.h -- C ABI of the B200-native Eager K-truss engine (libktg.so).
+ *
+ * This is the drop-in boundary for the reference's hot path. The reference
+ * (/root/reference/proj) exposes it as a C++ static-library API; each ktg_*
+ * entry point below replaces one of those functions with identical argument
+ * meaning, in-place mutation rules and error behaviour (errors come back as
+ * status codes; the C++ shim paper_2009_07929_b200/shim/ktruss_shim.cpp and
+ * the Python host layer paper_2009_07929_b200/truss.py rethrow them as the
+ * reference's exception types):
+ *
+ *   ktg_compute_supports  <- ktruss::compute_supports   include/ktruss/support.hpp:52-54,
+ *                                                       src/support.cpp:93-132
+ *   ktg_reset_supports    <- ktruss::reset_supports     support.hpp:56, support.cpp:134-136
+ *   ktg_intersect_tails   <- ktruss::intersect_tails    support.hpp:44-45, support.cpp:64-91
+ *   ktg_prune_edges       <- ktruss::prune_edges        include/ktruss/truss.hpp:38-39,
+ *                                                       src/truss.cpp:9-37
+ *   ktg_run_fixpoint      <- ktruss::detail::run_fixpoint truss.hpp:62-63, truss.cpp:41-53
+ *   ktg_ktruss            <- ktruss::ktruss             truss.hpp:44-45, truss.cpp:57-71
+ *   ktg_kmax_search       <- ktruss::kmax_search        truss.hpp:56, truss.cpp:73-103
+ *
+ * Data model (csr.hpp:17-23): upper-triangular zero-terminated CSR; vertex
+ * ids 1..n, 0 is the sentinel; row_ptr has n+2 u32 entries, col_idx has
+ * `slots` u32 entries; supports has one u32 per slot.
+ *
+ * All pointers in the ktg_* calls above are HOST pointers (like the
+ * reference's std::vectors); host<->device copies happen inside. The
+ * ktg_engine_* calls keep a graph resident in HBM across calls (the
+ * device-resident path the benchmark times).
+ *
+ * Threading: calls on distinct engines may run concurrently; one engine must
+ * not be used from two threads at once. No call retains caller pointers.
+ */
+#ifndef KTG_H
+#define KTG_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum {
+  KTG_OK = 0,
+  KTG_ERR_INVALID_PARAMETER = 1, /* ktruss::InvalidParameterError            */
+  KTG_ERR_SUPPORT_OVERFLOW = 2,  /* ktruss::SupportOverflowError; slot via ktg_last_error_slot() */
+  KTG_ERR_INVALID_INPUT = 3,     /* ktruss::InvalidInputError                */
+  KTG_ERR_CUDA = 5,              /* CUDA runtime / NCCL failure              */
+  KTG_ERR_NO_DEVICE = 6,         /* no usable sm_100 device                  */
+  KTG_ERR_OOM = 7                /* device or host allocation failed         */
+} ktg_status;
+
+/* Per-round observer (truss.hpp:25-26): called on the calling thread after
+ * every prune with HOST copies of the pruned col_idx and the supports that
+ * drove the round. Test-only: it forces a host-driven loop with a D2H copy
+ * per round. */
+typedef void (*ktg_round_cb)(const uint32_t* col_idx, const uint32_t* supports, uint64_t slots,
+                             uint64_t removed, void* user);
+
+/* Strategy (support.hpp:12-16). Every value runs the same device path; the
+ * results are identical by the reference's own contract. */
+enum { KTG_STRATEGY_SERIAL = 0, KTG_STRATEGY_COARSE = 1, KTG_STRATEGY_FINE = 2 };
+
+/* flags */
+enum {
+  KTG_FLAG_HOST_LOOP = 1u << 0,     /* host-driven fixpoint loop instead of the
+                                       device-resident CUDA-graph while loop  */
+  KTG_FLAG_NAIVE_SUPPORT = 1u << 1, /* thread-per-slot merge kernel (paper
+                                       Listing 1), for cross-checking only    */
+  KTG_FLAG_COLLECT_WORK = 1u << 2   /* record per-round closed-form work L_r,
+                                       live edges and triangles (extra kernels) */
+};
+
+typedef struct {
+  uint32_t struct_size;   /* sizeof(ktg_options)                              */
+  int32_t device;         /* CUDA ordinal; -1 = current device                */
+  uint32_t strategy;      /* KTG_STRATEGY_*; accepted, see above              */
+  uint32_t width_bits;    /* 32 (SupportWidth::Bits32) or 16 (Bits16)         */
+  uint32_t flags;         /* KTG_FLAG_*                                       */
+  void* stream;           /* cudaStream_t to run on; NULL = engine-owned      */
+  ktg_round_cb observer;  /* optional, test-only                             */
+  void* observer_user;
+} ktg_options;
+
+/* Fills *o with the defaults (device -1, Fine, 32-bit, no flags). */
+void ktg_options_init(ktg_options* o);
+
+/* Message / overflow slot of the last failing call on this thread. */
+const char* ktg_last_error(void);
+uint64_t ktg_last_error_slot(void);
+
+/* Library / device probe: 1 if an sm_100 device is visible, else 0. */
+int ktg_device_available(void);
+const char* ktg_version(void);
+
+/* ---------------------------------------------------------------------- */
+/* Reference-shaped entry points (host buffers)                            */
+/* ---------------------------------------------------------------------- */
+
+/* compute_supports: adds each live slot's triangle count into supports
+ * (which the reference requires to be zero on entry) and returns the
+ * triangle total. width_bits 16 -> KTG_ERR_SUPPORT_OVERFLOW naming the first
+ * slot above 65535 (support.cpp:53-60). s_len must equal slots. */
+ktg_status ktg_compute_supports(const uint32_t* row_ptr, uint32_t n, const uint32_t* col_idx,
+                                uint64_t slots, uint32_t* supports, uint64_t s_len,
+                                const ktg_options* opt, uint64_t* triangles);
+
+/* reset_supports: zero-fills supports[0..s_len). */
+void ktg_reset_supports(uint32_t* supports, uint64_t s_len);
+
+/* intersect_tails: merge of the pivot row tail with the predecessor's row;
+ * bumps both matching slots in supports, returns the match count in *found. */
+ktg_status ktg_intersect_tails(const uint32_t* row_ptr, uint32_t n, const uint32_t* col_idx,
+                               uint64_t slots, uint32_t pivot_slot, uint32_t predecessor,
+                               uint32_t* supports, uint32_t* found);
+
+/* prune_edges: in-place stable per-row compaction of col_idx keeping slots
+ * with supports >= k-2; returns the removed count. supports is not touched.
+ * k < 2 or s_len != slots -> KTG_ERR_INVALID_PARAMETER. */
+ktg_status ktg_prune_edges(const uint32_t* row_ptr, uint32_t n, uint32_t* col_idx, uint64_t slots,
+                           const uint32_t* supports, uint64_t s_len, uint32_t k,
+                           const ktg_options* opt, uint64_t* removed);
+
+/* detail::run_fixpoint: {reset, compute, prune} until a round removes
+ * nothing, mutating col_idx and supports in place (supports ends as the
+ * converged round's counts). Writes min(iterations, hist_cap) removal counts
+ * to removed_hist; the last is 0. */
+ktg_status ktg_run_fixpoint(const uint32_t* row_ptr, uint32_t n, uint32_t* col_idx, uint64_t slots,
+                            uint32_t* supports, uint64_t s_len, uint32_t k, const ktg_options* opt,
+                            uint64_t* removed_hist, uint32_t hist_cap, uint32_t* iterations);
+
+/* ktruss: fixpoint on a private copy (col_idx is not mutated); the surviving
+ * edges come back as parallel (u, v, support) arrays in lexicographic order
+ * (extract_edges, csr.cpp:93-106). edge_cap must be >= the live edge count
+ * of the input; *num_edges receives the survivor count. */
+ktg_status ktg_ktruss(const uint32_t* row_ptr, uint32_t n, const uint32_t* col_idx, uint64_t slots,
+                      uint32_t k, const ktg_options* opt, uint32_t* out_u, uint32_t* out_v,
+                      uint32_t* out_support, uint64_t edge_cap, uint64_t* num_edges,
+                      uint64_t* removed_hist, uint32_t hist_cap, uint32_t* iterations);
+
+/* kmax_search: largest k with a non-empty k-truss, plus that truss (same
+ * output convention as ktg_ktruss). Empty graph -> KTG_ERR_INVALID_PARAMETER. */
+ktg_status ktg_kmax_search(const uint32_t* row_ptr, uint32_t n, const uint32_t* col_idx,
+                           uint64_t slots, const ktg_options* opt, uint32_t* k_max,
+                           uint32_t* out_u, uint32_t* out_v, uint32_t* out_support,
+                           uint64_t edge_cap, uint64_t* num_edges, uint64_t* removed_hist,
+                           uint32_t hist_cap, uint32_t* iterations);
+
+/* ---------------------------------------------------------------------- */
+/* Device-resident engine                                                  */
+/* ---------------------------------------------------------------------- */
+
+typedef struct ktg_engine ktg_engine;
+
+typedef struct {
+  uint32_t iterations;       /* rounds of the last fixpoint                  */
+  uint64_t live_edges;       /* survivors after the last fixpoint            */
+  uint64_t triangles;        /* triangle total of the converged round        */
+  uint32_t max_support;      /* max S of the first round (kmax bound)        */
+  double device_ms;          /* CUDA-event time of the last run              */
+} ktg_run_info;
+
+/* Per-round closed-form work, recorded with KTG_FLAG_COLLECT_WORK. */
+typedef struct {
+  uint64_t live_edges;  /* live edges entering the round            */
+  uint64_t L;           /* sum_v d+(d+-1)/2 + d+ d-    */
+  uint64_t triangles;   /* triangles found in the round              */
+  uint64_t removed;     /* edges pruned by the round                 */
+} ktg_round_work;
+
+ktg_status ktg_engine_create(const ktg_options* opt, ktg_engine** out);
+void ktg_engine_destroy(ktg_engine* e);
+
+/* Uploads a graph (host pointers) and keeps a pristine copy in HBM. */
+ktg_status ktg_engine_load(ktg_engine* e, const uint32_t* row_ptr, uint32_t n,
+                           const uint32_t* col_idx, uint64_t slots);
+/* Same, from device pointers (D2D). */
+ktg_status ktg_engine_load_device(ktg_engine* e, const uint32_t* d_row_ptr, uint32_t n,
+                                  const uint32_t* d_col_idx, uint64_t slots);
+/* Restores the pristine col_idx and zeroes both support buffers (async on
+ * the engine stream). */
+ktg_status ktg_engine_reset(ktg_engine* e);
+/* Runs the fixpoint at k on the resident graph (from its current state).
+ * Asynchronous unless removed_hist/iterations are requested: pass NULL/0 to
+ * leave the result on the device and just enqueue. */
+ktg_status ktg_engine_run(ktg_engine* e, uint32_t k, uint64_t* removed_hist, uint32_t hist_cap,
+                          uint32_t* iterations);
+/* One support pass (no reset, no prune) over the resident graph into the
+ * current support buffer; optional triangle total (synchronises). */
+ktg_status ktg_engine_support_pass(ktg_engine* e, uint64_t* triangles);
+ktg_status ktg_engine_sync(ktg_engine* e);
+ktg_status ktg_engine_info(ktg_engine* e, ktg_run_info* info);
+/* Per-round work of the last run (needs KTG_FLAG_COLLECT_WORK). Returns the
+ * number of rounds written. */
+uint32_t ktg_engine_round_work(ktg_engine* e, ktg_round_work* out, uint32_t cap);
+/* Copies the current col_idx / supports (converged buffer) to host. */
+ktg_status ktg_engine_read(ktg_engine* e, uint32_t* col_idx, uint32_t* supports);
+/* Device pointers of the current state and the engine stream. */
+ktg_status ktg_engine_device_state(ktg_engine* e, uint32_t** d_col_idx, uint32_t** d_supports,
+                                   void** stream);
+/* Survivors of the resident graph as (u, v, support), lexicographic; device
+ * compaction, D2H of the survivors only. */
+ktg_status ktg_engine_extract(ktg_engine* e, uint32_t* out_u, uint32_t* out_v,
+                              uint32_t* out_support, uint64_t edge_cap, uint64_t* num_edges);
+
+/* Multi-GPU: this engine computes supports for its share of
+ * the support tasks only (work-balanced split into `world` parts); the
+ * caller all-reduces the support buffer between the support and prune steps
+ * through the allreduce callback, invoked once per round on the engine stream
+ * (host-driven loop). world == 1 restores single-GPU operation. */
+typedef int (*ktg_allreduce_cb)(uint32_t* d_buf, uint64_t count, void* stream, void* user);
+ktg_status ktg_engine_set_partition(ktg_engine* e, uint32_t rank, uint32_t world,
+                                    ktg_allreduce_cb allreduce, void* user);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

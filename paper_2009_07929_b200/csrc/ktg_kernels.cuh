@@ -1,0 +1,750 @@
+// Device kernels of the B200 Eager K-truss engine (sm_100a).
+//
+// Hot path per round:
+//   k_plan_count / k_plan_write  -- split the slot space into support tasks
+//   k_support_chunked            -- computeSupports (support.cpp:93-132 semantics)
+//   k_prune_light / k_prune_heavy-- pruneEdges (truss.cpp:9-37) fused with the
+//                                   support reset of the next round
+//   k_control                    -- removal history + device-side while flag
+//                                   (run_fixpoint, truss.cpp:41-53)
+//
+// All arithmetic is integer; every count the reference keeps in u64 is u64
+// here. Support increments are commutative atomics, so the result is
+// bit-identical to the reference for any schedule.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace ktg {
+
+constexpr int kChunk = 1024;         // slots per staged chunk (P)
+constexpr int kSupportThreads = 256; // threads per support CTA
+constexpr int kPruneThreads = 256;
+constexpr int kHeavyRow = 2048;      // rows longer than this are pruned by a CTA
+constexpr uint32_t kClipMin = 16;    // clip N+(j) by binary search above this degree
+constexpr uint32_t kScanRatio = 8;   // scan N+(j) if |N+(j)| <= ratio * |tail|
+constexpr int kHistCap = 1 << 16;    // recorded rounds per fixpoint
+
+// Device-resident loop state (one per engine).
+struct DevState {
+  unsigned long long removed;        // edges pruned this round
+  unsigned long long triangles;      // triangles found this round
+  unsigned long long last_triangles; // triangles of the last completed round
+  unsigned long long live;           // live edges
+  unsigned long long overflow_slot;  // min slot with S > 65535 (Bits16)
+  unsigned int parity;               // support buffer of the current round
+  unsigned int iter;                 // completed rounds
+  unsigned int threshold;            // k - 2
+  unsigned int task_next;            // support work counter
+  unsigned int npairs;               // off-diagonal tasks this round
+  unsigned int nheavy;               // heavy rows queued for CTA prune
+  unsigned int error;                // nonzero stops the loop
+  unsigned int max_support;          // max S seen by k_max_support
+  unsigned int width16;              // check supports against 65535
+  unsigned int pad;
+};
+
+struct Graph {
+  const uint32_t* row_ptr;  // n+2
+  uint32_t* col;            // slots (+pad)
+  uint32_t* S0;             // support buffers (ping-pong)
+  uint32_t* S1;
+  uint32_t* deg;            // live out-degree per row, n+2
+  const uint32_t* chunk_row;// row containing the last slot of each chunk
+  uint2* pairs;             // off-diagonal tasks (q, q2)
+  uint32_t* pair_counts;    // per-chunk off-diagonal task count
+  uint32_t* heavy_rows;     // rows queued for CTA prune
+  DevState* st;
+  unsigned long long* hist; // removal count per round
+  uint32_t n;
+  uint32_t nchunks;
+  uint64_t slots;
+  uint32_t rank;            // multi-GPU task split
+  uint32_t world;
+};
+
+__host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
+
+__device__ __forceinline__ uint32_t* cur_S(const Graph& g) { return g.st->parity ? g.S1 : g.S0; }
+__device__ __forceinline__ uint32_t* other_S(const Graph& g) { return g.st->parity ? g.S0 : g.S1; }
+
+__device__ __forceinline__ uint32_t lower_bound_g(const uint32_t* __restrict__ a, uint32_t lo, uint32_t hi,
+                                                  uint32_t key) {
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (__ldg(a + mid) < key) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+__device__ __forceinline__ uint32_t upper_bound_g(const uint32_t* __restrict__ a, uint32_t lo, uint32_t hi,
+                                                  uint32_t key) {
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (__ldg(a + mid) <= key) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// ---------------------------------------------------------------------------
+// Setup kernels
+// ---------------------------------------------------------------------------
+
+// Live out-degree of every row (position of the first zero; rows are
+// zero-prefix-free, csr.hpp:12-16) and the live total. Warp per row.
+__global__ void k_init_deg(const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ col,
+                           uint32_t n, uint32_t* __restrict__ deg, DevState* st) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  unsigned long long live = 0;
+  for (uint32_t v = warp + 1; v <= n; v += nwarps) {
+    const uint32_t b = row_ptr[v], e = row_ptr[v + 1];
+    uint32_t d = e - b;  // if no zero found (invalid CSR) fall back to the span
+    for (uint32_t off = b; off < e; off += 32) {
+      const uint32_t x = off + lane;
+      const bool z = x < e && col[x] == 0;
+      const unsigned m = __ballot_sync(0xffffffffu, z);
+      if (m) {
+        d = off + __ffs(m) - 1 - b;
+        break;
+      }
+    }
+    if (lane == 0) {
+      deg[v] = d;
+      live += d;
+    }
+  }
+  if (lane == 0 && live) atomicAdd(&st->live, live);
+  if (blockIdx.x == 0 && threadIdx.x == 0) deg[0] = 0;
+}
+
+// Row containing the last slot of every chunk (fixed for the graph's life).
+__global__ void k_chunk_rows(const uint32_t* __restrict__ row_ptr, uint32_t n, uint64_t slots,
+                             uint32_t nchunks, uint32_t* __restrict__ chunk_row) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nchunks) return;
+  const uint64_t e64 = umin64((uint64_t)(q + 1) * kChunk, slots) - 1;
+  const uint32_t e = (uint32_t)e64;
+  // upper_bound(row_ptr[0..n+2), e) - 1
+  uint32_t lo = 0, hi = n + 2;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (row_ptr[mid] <= e) lo = mid + 1; else hi = mid;
+  }
+  chunk_row[q] = lo - 1;
+}
+
+// ---------------------------------------------------------------------------
+// Planning: task list for the support kernel
+// ---------------------------------------------------------------------------
+// A task (q, q2) processes the pivots of chunk q against the a12 tails that
+// lie in chunk q2 (staged in shared memory). Diagonal tasks (q, q) cover every
+// pivot whose tail starts in its own chunk; only the last row of chunk q can
+// extend past it, and its pivots get one off-diagonal task per further chunk
+// its live part reaches.
+
+__global__ void k_plan_count(Graph g) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= g.nchunks) return;
+  const uint32_t i = g.chunk_row[q];
+  uint32_t cnt = 0;
+  if (i >= 1) {
+    const uint64_t le = (uint64_t)g.row_ptr[i] + g.deg[i];  // live end (exclusive)
+    const uint64_t e = umin64((uint64_t)(q + 1) * kChunk, g.slots);
+    if (le > e) cnt = (uint32_t)((le - 1) / kChunk - q);
+  }
+  g.pair_counts[q] = cnt;
+}
+
+// Single CTA: exclusive scan of pair_counts, write the pair list, reset the
+// task counter. 1024 threads.
+__global__ void __launch_bounds__(1024) k_plan_write(Graph g) {
+  __shared__ uint32_t warp_sums[32];
+  const uint32_t tid = threadIdx.x;
+  const uint32_t Q = g.nchunks;
+  const uint32_t per = (Q + blockDim.x - 1) / blockDim.x;
+  const uint32_t lo = min(tid * per, Q), hi = min(lo + per, Q);
+  uint32_t local = 0;
+  for (uint32_t q = lo; q < hi; ++q) local += g.pair_counts[q];
+  // block exclusive scan of `local`
+  const int lane = tid & 31, wid = tid >> 5;
+  uint32_t x = local;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) warp_sums[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t w = lane < (int)(blockDim.x >> 5) ? warp_sums[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    warp_sums[lane] = w;  // inclusive
+  }
+  __syncthreads();
+  uint32_t off = x - local + (wid ? warp_sums[wid - 1] : 0);
+  for (uint32_t q = lo; q < hi; ++q) {
+    const uint32_t c = g.pair_counts[q];
+    for (uint32_t t = 1; t <= c; ++t) g.pairs[off++] = make_uint2(q, q + t);
+  }
+  if (tid == blockDim.x - 1) {
+    g.st->npairs = off;
+    g.st->task_next = 0;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Support kernel
+// ---------------------------------------------------------------------------
+struct SupportSmem {
+  uint32_t A[kChunk];        // staged slots col[a0 .. a0+alen)
+  uint32_t cntA[kChunk];     // pending increments of staged slots
+  uint32_t cntP[kChunk];     // pending pivot counts (off-diagonal tasks)
+  uint32_t pref[kChunk + 1]; // exclusive prefix of per-pivot cost
+  uint32_t b0[kChunk];       // clipped N+(j) range [b0, b1)
+  uint32_t b1[kChunk];
+  uint16_t nz[kChunk];       // next zero at or after x (alen if none)
+  uint16_t tb[kChunk];       // tail range [tb, te) relative to a0
+  uint16_t te[kChunk];
+  uint8_t mode[kChunk];      // 1 = scan N+(j), 0 = iterate the tail
+  uint32_t red[kSupportThreads / 32];
+  uint32_t task;
+};
+
+// Block-wide exclusive scan of one u32 per thread; returns the prefix, total
+// in *total. Uses s.red as scratch.
+__device__ __forceinline__ uint32_t block_exscan(uint32_t v, uint32_t* red, uint32_t* total) {
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  constexpr int NW = kSupportThreads / 32;
+  uint32_t x = v;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) red[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t w = lane < NW ? red[lane] : 0;
+#pragma unroll
+    for (int o = 1; o < NW; o <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+      if (lane >= o) w += y;
+    }
+    if (lane < NW) red[lane] = w;
+  }
+  __syncthreads();
+  const uint32_t r = x - v + (wid ? red[wid - 1] : 0);
+  *total = red[NW - 1];
+  __syncthreads();
+  return r;
+}
+
+// Persistent CTAs pull tasks (q, q2) off a counter. Per task:
+//   1. stage chunk q2 of col in smem, find the next zero of every position;
+//   2. per pivot slot s=(i,j) in chunk q: its a12 tail within the staged chunk
+//      [tb, te); clip N+(j) to the tail's value range; choose SCAN (read
+//      N+(j) coalesced, binary-search each element in the smem tail) or
+//      ITERATE (binary-search each tail element in N+(j)) by cost;
+//   3. flatten all pivots' work with a prefix sum and split it evenly over
+//      the warps; each lane does one element per step;
+//   4. a match (i,j,k) adds 1 to S[slot(i,k)] (smem), S[slot(j,k)] (global
+//      red.add) and the pivot's count (smem); smem counts are flushed once.
+// Semantically each pivot slot gets exactly intersect_tails' matches
+// (support.cpp:64-91) plus the pivot add (support.cpp:122).
+__global__ void __launch_bounds__(kSupportThreads)
+k_support_chunked(Graph g) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SupportSmem& s = *reinterpret_cast<SupportSmem*>(smem_raw);
+  const uint32_t tid = threadIdx.x;
+  const int lane = tid & 31, wid = tid >> 5;
+  constexpr int NW = kSupportThreads / 32;
+  constexpr int EPT = kChunk / kSupportThreads;
+  uint32_t* __restrict__ S = cur_S(g);
+  const uint32_t* __restrict__ col = g.col;
+  const uint32_t npairs = g.st->npairs;
+  const uint32_t ntasks = npairs + g.nchunks;
+  unsigned long long tri_local = 0;
+
+  for (;;) {
+    if (tid == 0) s.task = atomicAdd(&g.st->task_next, 1u);
+    __syncthreads();
+    const uint32_t local = s.task;
+    const uint64_t t64 = (uint64_t)local * g.world + g.rank;
+    if (t64 >= ntasks) break;
+    const uint32_t t = (uint32_t)t64;
+    uint32_t q, q2;
+    if (t < npairs) {
+      const uint2 pr = g.pairs[t];
+      q = pr.x;
+      q2 = pr.y;
+    } else {
+      q = q2 = t - npairs;
+    }
+    const bool diag = q == q2;
+    const uint64_t a0 = (uint64_t)q2 * kChunk;
+    const uint32_t alen = (uint32_t)umin64(kChunk, g.slots - a0);
+    const uint64_t p0 = (uint64_t)q * kChunk;
+    const uint32_t plen = (uint32_t)umin64(kChunk, g.slots - p0);
+    uint32_t pstart = 0;
+    if (!diag) {
+      const uint32_t rs = g.row_ptr[g.chunk_row[q]];
+      pstart = rs > p0 ? (uint32_t)(rs - p0) : 0;
+    }
+
+    // 1. stage + zero counters
+    uint32_t first_zero = 0xffffffffu;
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      const uint32_t x = tid * EPT + e;
+      const uint32_t v = x < alen ? col[a0 + x] : 0u;
+      s.A[x] = v;
+      s.cntA[x] = 0;
+      s.cntP[x] = 0;
+      if (v == 0 && x < alen && first_zero == 0xffffffffu) first_zero = x;
+    }
+    // next-zero: exclusive suffix-min of first_zero over higher threads
+    {
+      uint32_t m = first_zero;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_down_sync(0xffffffffu, m, o);
+        if (lane + o < 32) m = min(m, y);
+      }
+      // m = min over lanes >= lane (inclusive) within warp
+      if (lane == 0) s.red[wid] = m;
+      __syncthreads();
+      uint32_t carry = 0xffffffffu;
+      for (int w = wid + 1; w < NW; ++w) carry = min(carry, s.red[w]);
+      const uint32_t incl_next = __shfl_down_sync(0xffffffffu, m, 1);
+      if (lane < 31) carry = min(carry, incl_next);
+      uint32_t cur = min(carry, alen);
+#pragma unroll
+      for (int e = EPT - 1; e >= 0; --e) {
+        const uint32_t x = tid * EPT + e;
+        if (x < alen && s.A[x] == 0) cur = x;
+        s.nz[x] = (uint16_t)min(cur, (uint32_t)kChunk);
+      }
+    }
+    __syncthreads();
+
+    // 2. per-pivot descriptors
+    uint32_t cost[EPT];
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      const uint32_t x = tid * EPT + e;
+      uint32_t c = 0;
+      if (x >= pstart && x < plen) {
+        const uint32_t j = diag ? s.A[x] : col[p0 + x];
+        const uint32_t tb_ = diag ? x + 1 : 0;
+        if (j != 0 && tb_ < alen) {
+          const uint32_t te_ = s.nz[tb_];
+          if (te_ > tb_) {
+            const uint32_t dj = g.deg[j];
+            if (dj) {
+              const uint32_t bs = g.row_ptr[j];
+              uint32_t b0_ = bs, b1_ = bs + dj;
+              if (dj > kClipMin) {
+                b0_ = lower_bound_g(col, bs, b1_, s.A[tb_]);
+                b1_ = upper_bound_g(col, b0_, b1_, s.A[te_ - 1]);
+              }
+              const uint32_t blen = b1_ - b0_;
+              if (blen) {
+                const uint32_t tlen = te_ - tb_;
+                const bool scan = blen <= tlen * kScanRatio;
+                c = scan ? blen : tlen;
+                s.b0[x] = b0_;
+                s.b1[x] = b1_;
+                s.tb[x] = (uint16_t)tb_;
+                s.te[x] = (uint16_t)te_;
+                s.mode[x] = scan;
+              }
+            }
+          }
+        }
+      }
+      cost[e] = c;
+    }
+    uint32_t mine = 0;
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) mine += cost[e];
+    uint32_t W;
+    uint32_t run = block_exscan(mine, s.red, &W);
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      s.pref[tid * EPT + e] = run;
+      run += cost[e];
+    }
+    if (tid == 0) s.pref[kChunk] = W;
+    __syncthreads();
+
+    // 3. flattened element work, contiguous range per warp
+    if (W) {
+      const uint32_t beg = (uint32_t)(((uint64_t)W * wid) / NW);
+      const uint32_t end = (uint32_t)(((uint64_t)W * (wid + 1)) / NW);
+      uint32_t f = beg + lane;
+      // first pivot with pref[p+1] > f
+      uint32_t p;
+      {
+        uint32_t lo = 0, hi = kChunk;
+        const uint32_t key = min(f, W - 1);
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (s.pref[mid + 1] <= key) lo = mid + 1; else hi = mid;
+        }
+        p = lo;
+      }
+      for (; f < end; f += 32) {
+        while (s.pref[p + 1] <= f) ++p;
+        const uint32_t o = f - s.pref[p];
+        bool hit = false;
+        if (s.mode[p]) {
+          const uint32_t pos = s.b0[p] + o;
+          const uint32_t k = col[pos];
+          uint32_t lo = s.tb[p], hi = s.te[p];
+          const uint32_t tend = hi;
+          while (lo < hi) {
+            const uint32_t mid = (lo + hi) >> 1;
+            if (s.A[mid] < k) lo = mid + 1; else hi = mid;
+          }
+          if (lo < tend && s.A[lo] == k) {
+            atomicAdd(&s.cntA[lo], 1u);
+            atomicAdd(&S[pos], 1u);
+            hit = true;
+          }
+        } else {
+          const uint32_t x = s.tb[p] + o;
+          const uint32_t k = s.A[x];
+          const uint32_t bend = s.b1[p];
+          const uint32_t y = lower_bound_g(col, s.b0[p], bend, k);
+          if (y < bend && __ldg(col + y) == k) {
+            atomicAdd(&s.cntA[x], 1u);
+            atomicAdd(&S[y], 1u);
+            hit = true;
+          }
+        }
+        if (hit) {
+          ++tri_local;
+          atomicAdd(diag ? &s.cntA[p] : &s.cntP[p], 1u);
+        }
+      }
+    }
+    __syncthreads();
+
+    // 4. flush smem counts
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      const uint32_t x = tid * EPT + e;
+      const uint32_t ca = s.cntA[x];
+      if (ca) atomicAdd(&S[a0 + x], ca);
+      if (!diag) {
+        const uint32_t cp = s.cntP[x];
+        if (cp) atomicAdd(&S[p0 + x], cp);
+      }
+    }
+    __syncthreads();
+  }
+
+  // triangle total (u64)
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) tri_local += __shfl_xor_sync(0xffffffffu, tri_local, o);
+  if (lane == 0 && tri_local) atomicAdd(&g.st->triangles, tri_local);
+}
+
+// Paper Listing 1 / support.cpp:115-127 as written: one thread per slot,
+// sequential two-pointer merge. Cross-check kernel only.
+__global__ void k_support_naive(Graph g) {
+  uint32_t* __restrict__ S = cur_S(g);
+  const uint32_t* __restrict__ col = g.col;
+  unsigned long long tri = 0;
+  for (uint64_t slot = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; slot < g.slots;
+       slot += (uint64_t)gridDim.x * blockDim.x) {
+    if ((slot % g.world) != g.rank) continue;
+    const uint32_t pred = col[slot];
+    if (pred == 0) continue;
+    uint32_t a = (uint32_t)slot + 1, b = g.row_ptr[pred], found = 0;
+    uint32_t ca = col[a], cb = col[b];
+    while (ca != 0 && cb != 0) {
+      if (ca == cb) {
+        atomicAdd(&S[a], 1u);
+        atomicAdd(&S[b], 1u);
+        ++found;
+        ca = col[++a];
+        cb = col[++b];
+      } else if (cb > ca) {
+        ca = col[++a];
+      } else {
+        cb = col[++b];
+      }
+    }
+    if (found) atomicAdd(&S[slot], found);
+    tri += found;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) tri += __shfl_xor_sync(0xffffffffu, tri, o);
+  if ((threadIdx.x & 31) == 0 && tri) atomicAdd(&g.st->triangles, tri);
+}
+
+// intersect_tails for one pivot (support.cpp:64-91), as written: the
+// single-slot unit-test surface of the reference API.
+__global__ void k_intersect_one(const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ col,
+                                uint32_t* __restrict__ S, uint32_t pivot, uint32_t pred, uint32_t* found) {
+  uint32_t a = pivot + 1, b = row_ptr[pred], f = 0;
+  while (col[a] != 0 && col[b] != 0) {
+    if (col[a] == col[b]) {
+      atomicAdd(&S[a], 1u);
+      atomicAdd(&S[b], 1u);
+      ++f;
+      ++a;
+      ++b;
+    } else if (col[b] > col[a]) {
+      ++a;
+    } else {
+      ++b;
+    }
+  }
+  *found = f;
+}
+
+// First slot whose support exceeds 65535 (check_16bit, support.cpp:53-60).
+__global__ void k_check16(Graph g) {
+  const uint32_t* __restrict__ S = cur_S(g);
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < g.slots;
+       x += (uint64_t)gridDim.x * blockDim.x) {
+    if (S[x] > 0xFFFFu) {
+      atomicMin(&g.st->overflow_slot, (unsigned long long)x);
+      g.st->error = 1;
+    }
+  }
+}
+
+__global__ void k_max_support(Graph g) {
+  const uint32_t* __restrict__ S = cur_S(g);
+  uint32_t m = 0;
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < g.slots;
+       x += (uint64_t)gridDim.x * blockDim.x)
+    m = max(m, S[x]);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(&g.st->max_support, m);
+}
+
+// ---------------------------------------------------------------------------
+// Prune (truss.cpp:9-37) fused with the next round's support reset
+// ---------------------------------------------------------------------------
+// Per row: stable compaction of live slots with S >= k-2 (ballot + popc),
+// zero-fill of the vacated tail, new live degree. With `fused_reset`:
+//   * the other support buffer (next round's) is zeroed over the row's live
+//     prefix -- the only slots the previous round could have written, since
+//     this row's vacated tail was zeroed when it was vacated;
+//   * the current buffer is zeroed over the vacated tail (a round that removes
+//     anything is not the converged one, so those counts are never returned).
+// Without it (host loop / observer) S is left untouched, as in the reference.
+__global__ void __launch_bounds__(kPruneThreads)
+k_prune_light(Graph g, int fused_reset) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  uint32_t* __restrict__ S = cur_S(g);
+  uint32_t* __restrict__ So = other_S(g);
+  uint32_t* __restrict__ col = g.col;
+  const uint32_t thr = g.st->threshold;
+  unsigned long long removed = 0;
+  for (uint32_t v = warp + 1; v <= g.n; v += nwarps) {
+    const uint32_t d = g.deg[v];
+    if (d == 0) continue;
+    if (d > (uint32_t)kHeavyRow) {
+      if (lane == 0) {
+        const uint32_t at = atomicAdd(&g.st->nheavy, 1u);
+        g.heavy_rows[at] = v;
+      }
+      continue;
+    }
+    const uint32_t base = g.row_ptr[v];
+    uint32_t write = 0;
+    for (uint32_t off = 0; off < d; off += 32) {
+      const uint32_t idx = off + lane;
+      const bool live = idx < d;
+      const uint32_t c = live ? col[base + idx] : 0u;
+      const uint32_t sv = live ? S[base + idx] : 0u;
+      const bool keep = live && sv >= thr;
+      const unsigned m = __ballot_sync(0xffffffffu, keep);
+      __syncwarp();  // every lane's loads precede any lane's in-place store
+      if (keep) col[base + write + __popc(m & ((1u << lane) - 1u))] = c;
+      if (fused_reset && live) So[base + idx] = 0;
+      write += __popc(m);
+    }
+    for (uint32_t x = write + lane; x < d; x += 32) {
+      col[base + x] = 0;
+      if (fused_reset) S[base + x] = 0;
+    }
+    if (lane == 0) {
+      g.deg[v] = write;
+      removed += d - write;
+    }
+  }
+  if (lane == 0 && removed) atomicAdd(&g.st->removed, removed);
+}
+
+// CTA per heavy row (queued by k_prune_light): same compaction with a
+// block-wide scan over tiles of 4 * kPruneThreads slots.
+__global__ void __launch_bounds__(kPruneThreads)
+k_prune_heavy(Graph g, int fused_reset) {
+  __shared__ uint32_t red[kPruneThreads / 32];
+  __shared__ uint32_t tot_s;
+  constexpr int EPT = 4;
+  constexpr int TILE = EPT * kPruneThreads;
+  const uint32_t tid = threadIdx.x;
+  const int lane = tid & 31, wid = tid >> 5;
+  constexpr int NW = kPruneThreads / 32;
+  uint32_t* __restrict__ S = cur_S(g);
+  uint32_t* __restrict__ So = other_S(g);
+  uint32_t* __restrict__ col = g.col;
+  const uint32_t thr = g.st->threshold;
+  const uint32_t nheavy = g.st->nheavy;
+  unsigned long long removed = 0;
+  for (uint32_t h = blockIdx.x; h < nheavy; h += gridDim.x) {
+    const uint32_t v = g.heavy_rows[h];
+    const uint32_t d = g.deg[v];
+    const uint32_t base = g.row_ptr[v];
+    uint32_t write = 0;
+    for (uint32_t off = 0; off < d; off += TILE) {
+      uint32_t c[EPT];
+      bool keep[EPT];
+      uint32_t cnt = 0;
+#pragma unroll
+      for (int e = 0; e < EPT; ++e) {
+        const uint32_t idx = off + tid * EPT + e;
+        const bool live = idx < d;
+        c[e] = live ? col[base + idx] : 0u;
+        const uint32_t sv = live ? S[base + idx] : 0u;
+        keep[e] = live && sv >= thr;
+        cnt += keep[e];
+        if (fused_reset && live) So[base + idx] = 0;
+      }
+      uint32_t x = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+      }
+      if (lane == 31) red[wid] = x;
+      __syncthreads();  // also: every thread has read its tile before writes
+      if (wid == 0) {
+        uint32_t w = lane < NW ? red[lane] : 0;
+#pragma unroll
+        for (int o = 1; o < NW; o <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+          if (lane >= o) w += y;
+        }
+        if (lane < NW) red[lane] = w;
+        if (lane == NW - 1) tot_s = w;
+      }
+      __syncthreads();
+      uint32_t pos = write + x - cnt + (wid ? red[wid - 1] : 0);
+#pragma unroll
+      for (int e = 0; e < EPT; ++e)
+        if (keep[e]) col[base + pos++] = c[e];
+      write += tot_s;
+      __syncthreads();
+    }
+    for (uint32_t x = write + tid; x < d; x += blockDim.x) {
+      col[base + x] = 0;
+      if (fused_reset) S[base + x] = 0;
+    }
+    if (tid == 0) {
+      g.deg[v] = write;
+      removed += d - write;
+    }
+    __syncthreads();
+  }
+  if (tid == 0 && removed) atomicAdd(&g.st->removed, removed);
+}
+
+// ---------------------------------------------------------------------------
+// Loop control
+// ---------------------------------------------------------------------------
+__global__ void k_begin(DevState* st, uint32_t threshold, uint32_t width16, int parity) {
+  st->removed = 0;
+  st->triangles = 0;
+  st->last_triangles = 0;
+  st->overflow_slot = ~0ull;
+  st->parity = parity < 0 ? (st->parity ^ 1u) : (unsigned)parity;
+  st->iter = 0;
+  st->threshold = threshold;
+  st->task_next = 0;
+  st->nheavy = 0;
+  st->error = 0;
+  st->max_support = 0;
+  st->width16 = width16;
+}
+
+// End of round: record removed, advance parity unless converged, and (graph
+// mode) set the while-node condition -- no host round trip per iteration.
+__global__ void k_control(DevState* st, unsigned long long* hist, cudaGraphConditionalHandle handle,
+                          int use_cond) {
+  const unsigned long long removed = st->removed;
+  const uint32_t it = st->iter;
+  if (it < (uint32_t)kHistCap) hist[it] = removed;
+  st->iter = it + 1;
+  st->live -= removed;
+  st->last_triangles = st->triangles;
+  st->triangles = 0;
+  st->removed = 0;
+  st->task_next = 0;
+  st->nheavy = 0;
+  const bool cont = removed != 0 && st->error == 0;
+  if (cont) st->parity ^= 1u;
+  if (use_cond) cudaGraphSetConditional(handle, cont ? 1u : 0u);
+}
+
+// ---------------------------------------------------------------------------
+// Per-round closed-form work, optional
+// ---------------------------------------------------------------------------
+__global__ void k_work_din(Graph g, uint32_t* __restrict__ din) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t v = warp + 1; v <= g.n; v += nwarps) {
+    const uint32_t d = g.deg[v], base = g.row_ptr[v];
+    for (uint32_t x = lane; x < d; x += 32) atomicAdd(&din[g.col[base + x]], 1u);
+  }
+}
+
+__global__ void k_work_L(Graph g, const uint32_t* __restrict__ din, unsigned long long* out) {
+  unsigned long long L = 0;
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x + 1; v <= g.n; v += gridDim.x * blockDim.x) {
+    const unsigned long long d = g.deg[v];
+    L += d * (d ? d - 1 : 0) / 2 + d * din[v];
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+  if ((threadIdx.x & 31) == 0 && L) atomicAdd(out, L);
+}
+
+// ---------------------------------------------------------------------------
+// Extraction (extract_edges, csr.cpp:93-106): survivors as (u, v, S)
+// ---------------------------------------------------------------------------
+__global__ void k_extract(Graph g, const unsigned long long* __restrict__ offs, uint32_t* __restrict__ u,
+                          uint32_t* __restrict__ v, uint32_t* __restrict__ sup) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t* __restrict__ S = cur_S(g);
+  for (uint32_t r = warp + 1; r <= g.n; r += nwarps) {
+    const uint32_t d = g.deg[r], base = g.row_ptr[r];
+    const unsigned long long o = offs[r];
+    for (uint32_t x = lane; x < d; x += 32) {
+      u[o + x] = r;
+      v[o + x] = g.col[base + x];
+      sup[o + x] = S[base + x];
+    }
+  }
+}
+
+}  // namespace ktg

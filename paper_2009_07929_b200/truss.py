@@ -1,0 +1,467 @@
+"""Host-side mirror of the reference K-truss API over the sm_100a engine.
+
+Same names, argument meaning and error behaviour as the reference C++ API
+(/root/reference/proj/include/ktruss/support.hpp and truss.hpp); every call
+goes through the C ABI of libktg.so (include/ktg.h). There is no CPU path:
+without the engine library or a B200 these functions raise.
+
+    compute_supports  support.hpp:52-54   support.cpp:93-132
+    reset_supports    support.hpp:56      support.cpp:134-136
+    intersect_tails   support.hpp:44-45   support.cpp:64-91
+    prune_edges       truss.hpp:38-39     truss.cpp:9-37
+    run_fixpoint      truss.hpp:62-63     truss.cpp:41-53
+    ktruss            truss.hpp:44-45     truss.cpp:57-71
+    kmax_search       truss.hpp:56        truss.cpp:73-103
+"""
+from __future__ import annotations
+
+import ctypes
+import enum
+import os
+from dataclasses import dataclass, field
+from typing import Callable, List, Optional
+
+import numpy as np
+
+from . import errors
+from ._lib import engine_lib
+from .graph import ZeroTerminatedCsr
+
+_vp = ctypes.c_void_p
+_u32 = ctypes.c_uint32
+_u64 = ctypes.c_uint64
+
+
+class Strategy(enum.IntEnum):
+    """support.hpp:12-16. All three run the same device path (identical
+    results are the reference's own contract)."""
+    Serial = 0
+    Coarse = 1
+    Fine = 2
+
+
+class SupportWidth(enum.IntEnum):
+    """support.hpp:21-24."""
+    Bits32 = 32
+    Bits16 = 16
+
+
+def to_string(s: Strategy) -> str:
+    """support.cpp:13-20."""
+    return {Strategy.Serial: "serial", Strategy.Coarse: "coarse", Strategy.Fine: "fine"}.get(s, "?")
+
+
+def strategy_from_string(name: str) -> Optional[Strategy]:
+    """support.cpp:22-27."""
+    return {"serial": Strategy.Serial, "coarse": Strategy.Coarse, "fine": Strategy.Fine}.get(name)
+
+
+def hardware_threads() -> int:
+    """support.cpp:29-32."""
+    return os.cpu_count() or 1
+
+
+@dataclass
+class SupportArray:
+    """support.hpp:28-35: one u32 counter per CSR slot."""
+    counts: np.ndarray
+
+    @classmethod
+    def zeros(cls, slot_count: int) -> "SupportArray":
+        return cls(np.zeros(slot_count, dtype=np.uint32))
+
+    def size(self) -> int:
+        return int(self.counts.shape[0])
+
+
+RoundObserver = Callable[[ZeroTerminatedCsr, SupportArray, int], None]
+
+
+@dataclass
+class TrussOptions:
+    """truss.hpp:28-33, plus engine flags (host_loop, naive_support) used by
+    tests to cross-check the device-resident loop and the optimised kernel."""
+    strategy: Strategy = Strategy.Fine
+    threads: int = 1
+    width: SupportWidth = SupportWidth.Bits32
+    observer: Optional[RoundObserver] = None
+    host_loop: bool = False
+    naive_support: bool = False
+    device: int = -1
+
+
+@dataclass
+class TrussResult:
+    """truss.hpp:12-21. `edges` is an (m, 3) u32 array of (u, v, support) in
+    lexicographic order (the reference's vector<SupportedEdge>)."""
+    k: int
+    edges: np.ndarray
+    iterations: int
+    removed_per_iteration: List[int]
+
+    def edge_tuples(self):
+        return [tuple(int(x) for x in r) for r in self.edges]
+
+
+@dataclass
+class KmaxResult:
+    """truss.hpp:47-50."""
+    k_max: int
+    truss: TrussResult
+
+
+# ---------------------------------------------------------------------------
+# ctypes plumbing
+# ---------------------------------------------------------------------------
+ROUND_CB = ctypes.CFUNCTYPE(None, ctypes.POINTER(_u32), ctypes.POINTER(_u32), _u64, _u64, _vp)
+ALLREDUCE_CB = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.POINTER(_u32), _u64, _vp, _vp)
+
+
+class _Options(ctypes.Structure):
+    _fields_ = [("struct_size", _u32), ("device", ctypes.c_int32), ("strategy", _u32),
+                ("width_bits", _u32), ("flags", _u32), ("stream", _vp),
+                ("observer", ROUND_CB), ("observer_user", _vp)]
+
+
+class _RunInfo(ctypes.Structure):
+    _fields_ = [("iterations", _u32), ("live_edges", _u64), ("triangles", _u64),
+                ("max_support", _u32), ("device_ms", ctypes.c_double)]
+
+
+class _RoundWork(ctypes.Structure):
+    _fields_ = [("live_edges", _u64), ("L", _u64), ("triangles", _u64), ("removed", _u64)]
+
+
+FLAG_HOST_LOOP = 1
+FLAG_NAIVE_SUPPORT = 2
+FLAG_COLLECT_WORK = 4
+
+_configured = False
+
+
+def lib():
+    global _configured
+    L = engine_lib()
+    if not _configured:
+        P = ctypes.POINTER
+        L.ktg_last_error.restype = ctypes.c_char_p
+        L.ktg_last_error_slot.restype = _u64
+        L.ktg_version.restype = ctypes.c_char_p
+        L.ktg_device_available.restype = ctypes.c_int
+        L.ktg_options_init.argtypes = [P(_Options)]
+        L.ktg_compute_supports.argtypes = [_vp, _u32, _vp, _u64, _vp, _u64, P(_Options), P(_u64)]
+        L.ktg_reset_supports.argtypes = [_vp, _u64]
+        L.ktg_intersect_tails.argtypes = [_vp, _u32, _vp, _u64, _u32, _u32, _vp, P(_u32)]
+        L.ktg_prune_edges.argtypes = [_vp, _u32, _vp, _u64, _vp, _u64, _u32, P(_Options), P(_u64)]
+        L.ktg_run_fixpoint.argtypes = [_vp, _u32, _vp, _u64, _vp, _u64, _u32, P(_Options), _vp, _u32,
+                                       P(_u32)]
+        L.ktg_ktruss.argtypes = [_vp, _u32, _vp, _u64, _u32, P(_Options), _vp, _vp, _vp, _u64, P(_u64),
+                                 _vp, _u32, P(_u32)]
+        L.ktg_kmax_search.argtypes = [_vp, _u32, _vp, _u64, P(_Options), P(_u32), _vp, _vp, _vp, _u64,
+                                      P(_u64), _vp, _u32, P(_u32)]
+        L.ktg_engine_create.argtypes = [P(_Options), P(_vp)]
+        L.ktg_engine_destroy.argtypes = [_vp]
+        L.ktg_engine_load.argtypes = [_vp, _vp, _u32, _vp, _u64]
+        L.ktg_engine_load_device.argtypes = [_vp, _vp, _u32, _vp, _u64]
+        L.ktg_engine_reset.argtypes = [_vp]
+        L.ktg_engine_run.argtypes = [_vp, _u32, _vp, _u32, P(_u32)]
+        L.ktg_engine_support_pass.argtypes = [_vp, P(_u64)]
+        L.ktg_engine_sync.argtypes = [_vp]
+        L.ktg_engine_info.argtypes = [_vp, P(_RunInfo)]
+        L.ktg_engine_round_work.argtypes = [_vp, P(_RoundWork), _u32]
+        L.ktg_engine_round_work.restype = _u32
+        L.ktg_engine_read.argtypes = [_vp, _vp, _vp]
+        L.ktg_engine_device_state.argtypes = [_vp, P(_vp), P(_vp), P(_vp)]
+        L.ktg_engine_extract.argtypes = [_vp, _vp, _vp, _vp, _u64, P(_u64)]
+        L.ktg_engine_set_partition.argtypes = [_vp, _u32, _u32, ALLREDUCE_CB, _vp]
+        _configured = True
+    return L
+
+
+def _check(rc: int) -> None:
+    if rc == 0:
+        return
+    L = lib()
+    msg = L.ktg_last_error().decode()
+    if rc == 1:
+        raise errors.InvalidParameterError(msg)
+    if rc == 2:
+        raise errors.SupportOverflowError(int(L.ktg_last_error_slot()), msg)
+    if rc == 3:
+        raise errors.InvalidInputError(msg)
+    if rc == 7:
+        raise MemoryError(msg)
+    raise errors.DeviceError(msg)
+
+
+def _p(a: np.ndarray) -> _vp:
+    return _vp(a.ctypes.data)
+
+
+def _u32arr(a) -> np.ndarray:
+    a = np.ascontiguousarray(a, dtype=np.uint32)
+    return a
+
+
+def _options(o: Optional[TrussOptions], keep=None) -> _Options:
+    c = _Options()
+    lib().ktg_options_init(ctypes.byref(c))
+    if o is None:
+        return c
+    c.strategy = int(o.strategy)
+    c.width_bits = int(o.width)
+    c.device = o.device
+    flags = 0
+    if o.host_loop:
+        flags |= FLAG_HOST_LOOP
+    if o.naive_support:
+        flags |= FLAG_NAIVE_SUPPORT
+    c.flags = flags
+    if o.observer is not None and keep is not None:
+        obs = o.observer
+        n_state = keep["graph"]
+
+        def tramp(col_p, s_p, slots, removed, _user):
+            col = np.ctypeslib.as_array(col_p, shape=(slots,)).copy()
+            sup = np.ctypeslib.as_array(s_p, shape=(slots,)).copy()
+            g = ZeroTerminatedCsr(n_state.num_vertices, n_state.row_ptr, col)
+            obs(g, SupportArray(sup), int(removed))
+
+        cb = ROUND_CB(tramp)
+        keep["cb"] = cb
+        c.observer = cb
+    return c
+
+
+def _check_threads(threads: int) -> None:
+    if threads < 1:
+        raise errors.InvalidParameterError("thread count must be >= 1")
+
+
+# ---------------------------------------------------------------------------
+# Reference API
+# ---------------------------------------------------------------------------
+
+def intersect_tails(graph: ZeroTerminatedCsr, pivot_slot: int, predecessor: int,
+                    supports: SupportArray) -> int:
+    """support.cpp:64-91. Mutates supports; returns the match count (the
+    caller owns the pivot add)."""
+    found = _u32()
+    col = _u32arr(graph.col_idx)
+    _check(lib().ktg_intersect_tails(_p(_u32arr(graph.row_ptr)), graph.num_vertices, _p(col),
+                                     col.shape[0], pivot_slot, predecessor, _p(supports.counts),
+                                     ctypes.byref(found)))
+    return int(found.value)
+
+
+def compute_supports(graph: ZeroTerminatedCsr, supports: SupportArray,
+                     strategy: Strategy = Strategy.Fine, threads: int = 1,
+                     width: SupportWidth = SupportWidth.Bits32) -> int:
+    """support.cpp:93-132: adds per-slot triangle counts into `supports`
+    (required zero on entry), returns the triangle total."""
+    _check_threads(threads)
+    if supports.counts.dtype != np.uint32 or not supports.counts.flags.c_contiguous:
+        supports.counts = _u32arr(supports.counts)
+    o = _options(TrussOptions(strategy=strategy, threads=threads, width=width))
+    tri = _u64()
+    col = _u32arr(graph.col_idx)
+    _check(lib().ktg_compute_supports(_p(_u32arr(graph.row_ptr)), graph.num_vertices, _p(col),
+                                      col.shape[0], _p(supports.counts), supports.size(),
+                                      ctypes.byref(o), ctypes.byref(tri)))
+    return int(tri.value)
+
+
+def reset_supports(supports: SupportArray) -> None:
+    """support.cpp:134-136."""
+    supports.counts[:] = 0
+
+
+def prune_edges(graph: ZeroTerminatedCsr, supports: SupportArray, k: int, threads: int = 1) -> int:
+    """truss.cpp:9-37: in-place stable compaction of graph.col_idx; returns
+    the removed count. supports is read only."""
+    if k < 2:
+        raise errors.InvalidParameterError("k must be >= 2")
+    _check_threads(threads)
+    if supports.size() != graph.total_slots():
+        raise errors.InvalidParameterError("support array does not match slot count")
+    graph.col_idx = _u32arr(graph.col_idx)
+    removed = _u64()
+    o = _options(None)
+    _check(lib().ktg_prune_edges(_p(_u32arr(graph.row_ptr)), graph.num_vertices, _p(graph.col_idx),
+                                 graph.total_slots(), _p(_u32arr(supports.counts)), supports.size(), k,
+                                 ctypes.byref(o), ctypes.byref(removed)))
+    return int(removed.value)
+
+
+def run_fixpoint(graph: ZeroTerminatedCsr, supports: SupportArray, k: int,
+                 options: Optional[TrussOptions] = None) -> List[int]:
+    """detail::run_fixpoint (truss.cpp:41-53): mutates graph.col_idx and
+    supports in place; returns the per-round removal counts (last is 0)."""
+    options = options or TrussOptions()
+    _check_threads(options.threads)
+    if supports.size() != graph.total_slots():
+        raise errors.InvalidParameterError("support array does not match slot count")
+    if k < 2:
+        raise errors.InvalidParameterError("k must be >= 2")
+    graph.col_idx = _u32arr(graph.col_idx)
+    supports.counts = _u32arr(supports.counts)
+    keep = {"graph": graph}
+    o = _options(options, keep)
+    cap = 1 << 16
+    hist = np.zeros(cap, dtype=np.uint64)
+    it = _u32()
+    _check(lib().ktg_run_fixpoint(_p(_u32arr(graph.row_ptr)), graph.num_vertices, _p(graph.col_idx),
+                                  graph.total_slots(), _p(supports.counts), supports.size(), k,
+                                  ctypes.byref(o), _p(hist), cap, ctypes.byref(it)))
+    return [int(x) for x in hist[:min(it.value, cap)]]
+
+
+def ktruss(graph: ZeroTerminatedCsr, k: int, options: Optional[TrussOptions] = None) -> TrussResult:
+    """truss.cpp:57-71: fixpoint on a private copy; survivors with their
+    converged supports."""
+    if k < 2:
+        raise errors.InvalidParameterError("k must be >= 2")
+    options = options or TrussOptions()
+    _check_threads(options.threads)
+    col = _u32arr(graph.col_idx)
+    live = int(np.count_nonzero(col))
+    cap_e = max(live, 1)
+    out = np.empty((3, cap_e), dtype=np.uint32)
+    num = _u64()
+    hcap = 1 << 16
+    hist = np.zeros(hcap, dtype=np.uint64)
+    it = _u32()
+    keep = {"graph": graph}
+    o = _options(options, keep)
+    _check(lib().ktg_ktruss(_p(_u32arr(graph.row_ptr)), graph.num_vertices, _p(col), col.shape[0], k,
+                            ctypes.byref(o), _p(out[0]), _p(out[1]), _p(out[2]), cap_e,
+                            ctypes.byref(num), _p(hist), hcap, ctypes.byref(it)))
+    m = int(num.value)
+    edges = np.ascontiguousarray(out[:, :m].T)
+    return TrussResult(k, edges, int(it.value), [int(x) for x in hist[:min(it.value, hcap)]])
+
+
+def kmax_search(graph: ZeroTerminatedCsr, options: Optional[TrussOptions] = None) -> KmaxResult:
+    """truss.cpp:73-103: largest k with a non-empty k-truss, and that truss."""
+    options = options or TrussOptions()
+    _check_threads(options.threads)
+    col = _u32arr(graph.col_idx)
+    live = int(np.count_nonzero(col))
+    cap_e = max(live, 1)
+    out = np.empty((3, cap_e), dtype=np.uint32)
+    num = _u64()
+    hcap = 1 << 16
+    hist = np.zeros(hcap, dtype=np.uint64)
+    it = _u32()
+    kmax = _u32()
+    keep = {"graph": graph}
+    o = _options(options, keep)
+    _check(lib().ktg_kmax_search(_p(_u32arr(graph.row_ptr)), graph.num_vertices, _p(col), col.shape[0],
+                                 ctypes.byref(o), ctypes.byref(kmax), _p(out[0]), _p(out[1]), _p(out[2]),
+                                 cap_e, ctypes.byref(num), _p(hist), hcap, ctypes.byref(it)))
+    m = int(num.value)
+    edges = np.ascontiguousarray(out[:, :m].T)
+    tr = TrussResult(int(kmax.value), edges, int(it.value), [int(x) for x in hist[:min(it.value, hcap)]])
+    return KmaxResult(int(kmax.value), tr)
+
+
+class detail:  # namespace ktruss::detail (truss.hpp:58-63)
+    run_fixpoint = staticmethod(run_fixpoint)
+
+
+# ---------------------------------------------------------------------------
+# Device-resident engine (what the benchmark times)
+# ---------------------------------------------------------------------------
+
+class Engine:
+    """A graph resident in HBM with its pristine copy; ktg_engine_* calls."""
+
+    def __init__(self, graph: Optional[ZeroTerminatedCsr] = None, options: Optional[TrussOptions] = None,
+                 collect_work: bool = False, stream: Optional[int] = None):
+        L = lib()
+        self._keep = {"graph": graph}
+        o = _options(options, self._keep)
+        if collect_work:
+            o.flags |= FLAG_COLLECT_WORK
+        if stream is not None:
+            o.stream = _vp(stream)
+        self._h = _vp()
+        _check(L.ktg_engine_create(ctypes.byref(o), ctypes.byref(self._h)))
+        self.graph = None
+        if graph is not None:
+            self.load(graph)
+
+    def close(self):
+        if self._h:
+            lib().ktg_engine_destroy(self._h)
+            self._h = _vp()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def load(self, graph: ZeroTerminatedCsr) -> None:
+        self.graph = graph
+        self._keep["graph"] = graph
+        rp, col = _u32arr(graph.row_ptr), _u32arr(graph.col_idx)
+        _check(lib().ktg_engine_load(self._h, _p(rp), graph.num_vertices, _p(col), col.shape[0]))
+
+    def load_device(self, d_row_ptr: int, n: int, d_col: int, slots: int) -> None:
+        _check(lib().ktg_engine_load_device(self._h, _vp(d_row_ptr), n, _vp(d_col), slots))
+
+    def reset(self) -> None:
+        _check(lib().ktg_engine_reset(self._h))
+
+    def run(self, k: int, sync: bool = True) -> Optional[List[int]]:
+        if not sync:
+            _check(lib().ktg_engine_run(self._h, k, None, 0, None))
+            return None
+        cap = 1 << 16
+        hist = np.zeros(cap, dtype=np.uint64)
+        it = _u32()
+        _check(lib().ktg_engine_run(self._h, k, _p(hist), cap, ctypes.byref(it)))
+        return [int(x) for x in hist[:min(it.value, cap)]]
+
+    def support_pass(self) -> int:
+        tri = _u64()
+        _check(lib().ktg_engine_support_pass(self._h, ctypes.byref(tri)))
+        return int(tri.value)
+
+    def sync(self) -> None:
+        _check(lib().ktg_engine_sync(self._h))
+
+    def info(self) -> dict:
+        i = _RunInfo()
+        _check(lib().ktg_engine_info(self._h, ctypes.byref(i)))
+        return {k: getattr(i, k) for k, _ in _RunInfo._fields_}
+
+    def round_work(self) -> List[dict]:
+        buf = (_RoundWork * (1 << 16))()
+        m = lib().ktg_engine_round_work(self._h, buf, 1 << 16)
+        return [{k: getattr(buf[i], k) for k, _ in _RoundWork._fields_} for i in range(m)]
+
+    def read(self):
+        slots = self.graph.total_slots()
+        col = np.empty(slots, dtype=np.uint32)
+        sup = np.empty(slots, dtype=np.uint32)
+        _check(lib().ktg_engine_read(self._h, _p(col), _p(sup)))
+        return col, sup
+
+    def device_state(self):
+        c, s, st = _vp(), _vp(), _vp()
+        _check(lib().ktg_engine_device_state(self._h, ctypes.byref(c), ctypes.byref(s), ctypes.byref(st)))
+        return c.value, s.value, st.value
+
+    def extract(self, cap: Optional[int] = None) -> np.ndarray:
+        cap = cap if cap is not None else max(1, self.graph.num_edges)
+        out = np.empty((3, cap), dtype=np.uint32)
+        num = _u64()
+        _check(lib().ktg_engine_extract(self._h, _p(out[0]), _p(out[1]), _p(out[2]), cap, ctypes.byref(num)))
+        return np.ascontiguousarray(out[:, :int(num.value)].T)
+
+    def set_partition(self, rank: int, world: int, allreduce=None) -> None:
+        cb = ALLREDUCE_CB(allreduce) if allreduce is not None else ALLREDUCE_CB()
+        self._keep["allreduce"] = cb
+        _check(lib().ktg_engine_set_partition(self._h, rank, world, cb, None))
