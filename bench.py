@@ -1,0 +1,408 @@
+#!/usr/bin/env python
+"""K-truss benchmark on B200 (one JSON line on rank 0).
+
+Workload (BASELINE.json configs[1]): R-MAT scale-20 edgefactor-16 (Graph500
+a/b/c, seed 42), K sweep 3..K_max. One step = the whole
+sweep, every K from the pristine graph exactly as the reference's
+ktruss(graph, k) would run it (truss.cpp:57-71) -- no state carried between
+K values. Metric: edges/s = (#K * m) / sweep time, m = original canonical
+edges (bench.cpp:45); time-to-fixpoint per K is reported alongside.
+
+  value    device-resident sweep: graph in HBM, per K a D2D restore of the
+           pristine col_idx + the device-side fixpoint (CUDA-graph while loop),
+           CUDA events on the engine stream, max over ranks.
+  e2e      the same sweep through the reference-shaped C ABI with HOST
+           buffers (ktg_ktruss: H2D of the CSR, fixpoint, D2H of the truss)
+           per K, from pinned memory.
+  roofline the support kernel (k_support_chunked): algorithmic bytes of
+           SURVEY.md §8(d) per launch / its CUDA-event duration (host-driven
+           instrumented pass, sampled K values).
+  cpu_baseline  the reference library itself (oracle/_ref, Strategy::Fine,
+           all host threads) on a bounded sample of the same sweep.
+
+--impl reference times only the reference CPU implementation (rank 0).
+Multi-GPU (torchrun): the K values are split across ranks (independent
+fixpoints on a replicated graph; no data-path collective), strong scaling.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "K-truss time-to-fixpoint (ms) & edges/sec at 1/2/4/8 B200; achieved HBM GB/s"
+# K_max of the pinned configs (reference-measured; also
+# asserted by tests/test_gpu_large.py) -- lets the reference arm skip its
+# ~200 s CPU kmax_search.
+KNOWN_KMAX = {(14, 16, 42): 79, (20, 16, 42): 304}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scale", type=int, default=20)
+    ap.add_argument("--ef", type=int, default=16)
+    ap.add_argument("--seed", type=int, default=42)
+    ap.add_argument("--kstride", type=int, default=1, help="K sweep stride (1 = every K)")
+    ap.add_argument("--e2e-steps", type=int, default=1)
+    ap.add_argument("--cpu-budget-s", type=float, default=20.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+class ClockSampler:
+    """nvidia-smi-equivalent clock / throttle sampling (NVML) during the timed
+    region."""
+
+    REASONS = {
+        0x0000000000000002: "applications_clocks",
+        0x0000000000000004: "sw_power_cap",
+        0x0000000000000008: "hw_slowdown",
+        0x0000000000000020: "sw_thermal_slowdown",
+        0x0000000000000040: "hw_thermal_slowdown",
+        0x0000000000000080: "hw_power_brake_slowdown",
+    }
+
+    def __init__(self, index: int):
+        self.samples, self.reasons, self.max_mhz = [], set(), None
+        self._stop = threading.Event()
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+        except Exception:  # pragma: no cover - NVML missing
+            self.nv = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                r = self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                for bit, name in self.REASONS.items():
+                    if r & bit:
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            self._stop.wait(0.1)
+
+    def __enter__(self):
+        if self.nv:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        if self.nv:
+            self.t.join()
+
+    def summary(self):
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": sorted(self.reasons),
+                "samples": len(self.samples)}
+
+
+def k_values(kmax: int, stride: int):
+    ks = list(range(3, kmax + 1, stride))
+    if ks[-1] != kmax:
+        ks.append(kmax)
+    return ks
+
+
+def support_bytes(w, n, slots):
+    """Algorithmic bytes of one support launch: list reads
+    4*L_r, pivot scan 4*slots, IA 4*(n+2), 3 atomic u32 per triangle."""
+    return 4 * w["L"] + 4 * slots + 4 * (n + 2) + 12 * w["triangles"]
+
+
+def fixpoint_bytes(work, n, slots):
+    """Per-fixpoint algorithmic bytes B of SURVEY.md §8(d) (support + the
+    16 B/slot prune)."""
+    return sum(support_bytes(w, n, slots) + 16 * slots for w in work)
+
+
+def cpu_sample(g, ks, budget_s, threads):
+    """The reference library (oracle/_ref) on a bounded, evenly spread sample
+    of the sweep's K values; every K from pristine; run_fixpoint timed only
+    (bench.cpp:33-40). Returns (edges/s, sample description, ms list)."""
+    import oracle
+    R = oracle.ref()
+    # spread: K=3 (heaviest), K_max, then bisecting the range
+    cand = [ks[0], ks[-1]]
+    step = max(1, len(ks) // 2)
+    while step >= 1 and len(cand) < len(ks):
+        for i in range(0, len(ks), step):
+            if ks[i] not in cand:
+                cand.append(ks[i])
+        step //= 2
+    t_total, done = 0.0, []
+    for k in cand:
+        _, _, _, ms = R.run_fixpoint(g, k, 2, threads)
+        done.append((k, ms))
+        t_total += ms / 1e3
+        if t_total >= budget_s:
+            break
+    m = g.num_edges
+    tot_ms = sum(ms for _, ms in done)
+    return m * len(done) / (tot_ms / 1e3), done
+
+
+def run_reference(args):
+    """--impl reference: the reference's own CPU implementation only."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import oracle
+    import paper_2009_07929_b200 as kt
+    g = kt.rmat(args.scale, args.ef, args.seed)
+    key = (args.scale, args.ef, args.seed)
+    if key not in KNOWN_KMAX:
+        print(json.dumps({"impl": "reference", "unavailable": f"no pinned K_max for {key}"}))
+        return
+    ks = k_values(KNOWN_KMAX[key], args.kstride)
+    R = oracle.ref()
+    threads = os.cpu_count() or 1
+    # evenly spread K order so any step count samples the whole sweep
+    order = []
+    stride = max(1, len(ks) // max(1, args.steps + args.warmup))
+    for off in range(stride):
+        order.extend(ks[off::stride])
+    times = []
+    for i in range(args.warmup + args.steps):
+        k = order[i % len(order)]
+        _, _, _, ms = R.run_fixpoint(g, k, 2, threads)
+        if i >= args.warmup:
+            times.append((k, ms))
+    mean_ms = sum(ms for _, ms in times) / len(times)
+    value = g.num_edges / (mean_ms / 1e3)
+    sample = f"one pristine fixpoint per step, K in {[k for k, _ in times]}"
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "edges/s",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": mean_ms,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+        "data": "synthetic",
+        "config": {"workload": f"rmat-s{args.scale}-ef{args.ef} K-sweep 3..{ks[-1]} (pristine per K)",
+                   "n": g.num_vertices, "m": g.num_edges, "k_values": len(ks), "parallelism": "cpu-omp"},
+        "cpu_baseline": {"value": value, "unit": "edges/s", "cores": threads, "kind": "reference",
+                         "sample": sample},
+        "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2009_07929_b200 as kt
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def allmax(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    def allsum(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.SUM)
+        return float(t.item())
+
+    t0 = time.time()
+    g = kt.rmat(args.scale, args.ef, args.seed)
+    gen_s = time.time() - t0
+    n, slots, m = g.num_vertices, g.total_slots(), g.num_edges
+
+    stream = torch.cuda.Stream()
+    eng = kt.Engine(g, stream=stream.cuda_stream)
+    kmax = eng.kmax()  # untimed, as run_bench resolves K_max (bench.cpp:25)
+    ks = k_values(kmax, args.kstride)
+    # K split across ranks: greedy by a cost proxy (K=3 is the heaviest)
+    mine = ks[rank::world]
+
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+
+    def sweep(kset):
+        for k in kset:
+            eng.reset()
+            eng.run(k, sync=False)
+
+    launches_per_k = {}
+    # one synchronous pass: iterations per K (for the launch count) + checks
+    for k in mine:
+        eng.reset()
+        h = eng.run(k)
+        launches_per_k[k] = 2 + 6 * len(h)  # k_set_live + k_begin + 6 per round
+
+    for _ in range(args.warmup):
+        sweep(mine)
+    torch.cuda.synchronize()
+
+    step_ms = []
+    barrier()
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.fill_(1)  # L2 flush between timed steps (not timed)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            sweep(mine)
+            e1.record(stream)
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+    torch.cuda.synchronize()
+    barrier()
+    ms_per_step = allmax(sum(step_ms) / len(step_ms))
+    total_k = len(ks)
+    value = total_k * m / (ms_per_step / 1e3)
+
+    # ---- end to end through the reference-shaped C ABI (host buffers) ----
+    pin_keep = (torch.empty(n + 2, dtype=torch.int32, pin_memory=True),
+                torch.empty(slots, dtype=torch.int32, pin_memory=True))
+    pin_rp = pin_keep[0].numpy().view(np.uint32)
+    pin_col = pin_keep[1].numpy().view(np.uint32)
+    pin_rp[:] = g.row_ptr
+    pin_col[:] = g.col_idx
+    hg = kt.ZeroTerminatedCsr(n, pin_rp, pin_col)
+    e2e_ms, d2h = [], 0
+    barrier()
+    for _ in range(max(1, args.e2e_steps)):
+        torch.cuda.synchronize()
+        t = time.perf_counter()
+        d2h = 0
+        for k in mine:
+            r = kt.ktruss(hg, k)
+            d2h += r.edges.nbytes + 8 * r.iterations
+        torch.cuda.synchronize()
+        e2e_ms.append((time.perf_counter() - t) * 1e3)
+    barrier()
+    e2e_step_ms = allmax(sum(e2e_ms) / len(e2e_ms))
+    h2d = allsum(len(mine) * (n + 2 + slots) * 4)
+    d2h = allsum(d2h)
+
+    # ---- roofline of the support kernel (instrumented, untimed) ----
+    roof = None
+    if rank == 0:
+        peaks = {}
+        try:
+            peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+            peak, peak_src = float(peaks["hbm_gbs"]), "measured"
+        except Exception:
+            peak, peak_src = 6650.0, "fallback"
+        sample_k = sorted(set([ks[0]] + ks[len(ks) // 4::max(1, len(ks) // 4)] + [ks[-1]]))
+        ew = kt.Engine(g, collect_work=True)
+        et = kt.Engine(g, time_support=True)
+        tot_b = tot_ms = 0.0
+        n_launch = 0
+        fix_b = 0.0
+        for k in sample_k:
+            ew.reset()
+            ew.run(k)
+            work = ew.round_work()
+            et.reset()
+            et.run(k)
+            tw = et.round_work()
+            for w, t in zip(work, tw):
+                tot_b += support_bytes(w, n, slots)
+                tot_ms += t["support_ms"]
+                n_launch += 1
+            fix_b += fixpoint_bytes(work, n, slots)
+        ew.close()
+        et.close()
+        achieved = tot_b / (tot_ms / 1e3) / 1e9
+        traffic = None
+        tp = os.path.join(ROOT, "profiles", "support_traffic.json")
+        if os.path.exists(tp):
+            try:
+                tj = json.load(open(tp))
+                traffic = tj.get(f"rmat-s{args.scale}-ef{args.ef}")
+            except Exception:
+                traffic = None
+        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": traffic,
+                "peak_source": peak_src, "kernel": "k_support_chunked",
+                "launches_measured": n_launch, "sample_k": sample_k,
+                "bytes_per_launch_avg": tot_b / max(1, n_launch),
+                "ms_per_launch_avg": tot_ms / max(1, n_launch)}
+
+    # ---- CPU baseline: the reference library on the host cores ----
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            threads = os.cpu_count() or 1
+            v, done = cpu_sample(g, ks, args.cpu_budget_s, threads)
+            cpu = {"value": v, "unit": "edges/s", "cores": threads, "kind": "reference",
+                   "sample": "reference run_fixpoint (Strategy::Fine) from pristine at K in "
+                             f"{[k for k, _ in done]} ({', '.join(f'{ms:.0f}' for _, ms in done)} ms)"}
+        except Exception as ex:  # reference library not built
+            cpu = {"value": None, "unit": "edges/s", "cores": 0, "kind": "reference",
+                   "sample": f"unavailable: {ex}"}
+
+    launches = args.steps * sum(launches_per_k.values())
+    launches = int(allsum(launches))
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "u32",
+            "data": "synthetic",
+            "config": {
+                "workload": f"rmat-s{args.scale}-ef{args.ef} K-sweep 3..{kmax} (pristine per K)",
+                "graph": f"R-MAT scale {args.scale} edgefactor {args.ef} seed {args.seed} "
+                         "(a,b,c)=(.57,.19,.19), Fisher-Yates relabel",
+                "n": n, "m": m, "slots": slots, "k_max": kmax, "k_values": total_k,
+                "kstride": args.kstride,
+                "l2": "512 MiB memset between timed steps (col_idx 65 MB < L2); per-K D2D restore",
+                "parallelism": f"k-split x{world}" if world > 1 else "single",
+            },
+            "time_to_fixpoint_ms_mean": ms_per_step / total_k * world,
+            "me_per_s": value / 1e6,
+            "e2e": {"value": total_k * m / (e2e_step_ms / 1e3), "unit": "edges/s",
+                    "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                    "ms_per_step": e2e_step_ms, "api": "ktg_ktruss (host buffers, pinned)"},
+            "roofline": roof,
+            "cpu_baseline": cpu,
+            "gpu_launches": launches,
+            "clocks": clocks.summary(),
+            "gen_s": round(gen_s, 2),
+        }
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

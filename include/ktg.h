@@ -67,8 +67,10 @@ enum {
                                        device-resident CUDA-graph while loop  */
   KTG_FLAG_NAIVE_SUPPORT = 1u << 1, /* thread-per-slot merge kernel (paper
                                        Listing 1), for cross-checking only    */
-  KTG_FLAG_COLLECT_WORK = 1u << 2   /* record per-round closed-form work L_r,
+  KTG_FLAG_COLLECT_WORK = 1u << 2,  /* record per-round closed-form work L_r,
                                        live edges and triangles (extra kernels) */
+  KTG_FLAG_TIME_SUPPORT = 1u << 3   /* host loop; CUDA events around every
+                                       support launch (ktg_round_work.support_ms) */
 };
 
 typedef struct {
@@ -166,6 +168,7 @@ typedef struct {
   uint64_t L;           /* sum_v d+(d+-1)/2 + d+ d-    */
   uint64_t triangles;   /* triangles found in the round              */
   uint64_t removed;     /* edges pruned by the round                 */
+  double support_ms;    /* support kernel time (KTG_FLAG_TIME_SUPPORT) */
 } ktg_round_work;
 
 ktg_status ktg_engine_create(const ktg_options* opt, ktg_engine** out);
@@ -190,7 +193,7 @@ ktg_status ktg_engine_run(ktg_engine* e, uint32_t k, uint64_t* removed_hist, uin
 ktg_status ktg_engine_support_pass(ktg_engine* e, uint64_t* triangles);
 ktg_status ktg_engine_sync(ktg_engine* e);
 ktg_status ktg_engine_info(ktg_engine* e, ktg_run_info* info);
-/* Per-round work of the last run (needs KTG_FLAG_COLLECT_WORK). Returns the
+/* Per-round records of the last run (KTG_FLAG_COLLECT_WORK / _TIME_SUPPORT). Returns the
  * number of rounds written. */
 uint32_t ktg_engine_round_work(ktg_engine* e, ktg_round_work* out, uint32_t cap);
 /* Copies the current col_idx / supports (converged buffer) to host. */

@@ -98,7 +98,7 @@ struct ktg_engine {
   ktg_allreduce_cb allreduce = nullptr;
   void* allreduce_user = nullptr;
 
-  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr, evs0 = nullptr, evs1 = nullptr;
   ktg_run_info info{};
   std::vector<ktg_round_work> work;
 
@@ -182,6 +182,8 @@ ktg_status engine_init(const ktg_options* opt, ktg_engine* e) {
   KTG_CUDA(cudaMallocHost(&e->h_st, sizeof(DevState)));
   KTG_CUDA(cudaEventCreate(&e->ev0));
   KTG_CUDA(cudaEventCreate(&e->ev1));
+  KTG_CUDA(cudaEventCreate(&e->evs0));
+  KTG_CUDA(cudaEventCreate(&e->evs1));
 
   e->support_smem = sizeof(SupportSmem);
   KTG_CUDA(cudaFuncSetAttribute(k_support_chunked, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -255,17 +257,20 @@ ktg_status engine_load(ktg_engine* e, const uint32_t* row_ptr, uint32_t n, const
 }
 
 // Enqueue one round: plan -> support -> [check16] -> [allreduce] -> prune -> control.
-ktg_status enqueue_round(ktg_engine* e, bool graph_mode, cudaGraphConditionalHandle handle) {
+ktg_status enqueue_round(ktg_engine* e, bool graph_mode, cudaGraphConditionalHandle handle,
+                         cudaEvent_t sup0 = nullptr, cudaEvent_t sup1 = nullptr) {
   Graph g = e->dev_graph();
   const cudaStream_t s = e->stream;
   const int fused = graph_mode ? 1 : 0;
   k_plan_count<<<(e->nchunks + 255) / 256, 256, 0, s>>>(g);
   k_plan_write<<<1, 1024, 0, s>>>(g);
+  if (sup0) KTG_CUDA(cudaEventRecord(sup0, s));
   if (flag(e, KTG_FLAG_NAIVE_SUPPORT)) {
     k_support_naive<<<4 * e->num_sms, 256, 0, s>>>(g);
   } else {
     k_support_chunked<<<e->support_grid, kSupportThreads, e->support_smem, s>>>(g);
   }
+  if (sup1) KTG_CUDA(cudaEventRecord(sup1, s));
   if (e->opt.width_bits == 16) k_check16<<<4 * e->num_sms, 256, 0, s>>>(g);
   KTG_CUDA(cudaGetLastError());
   if (!graph_mode && e->world > 1 && e->allreduce) {
@@ -358,8 +363,9 @@ ktg_status collect_work(ktg_engine* e, ktg_round_work* w) {
 
 // The fixpoint. Expects begin_run() already enqueued.
 ktg_status run_loop(ktg_engine* e, bool want_sync) {
-  const bool host_loop = flag(e, KTG_FLAG_HOST_LOOP) || e->opt.observer || (e->world > 1) ||
-                         flag(e, KTG_FLAG_COLLECT_WORK);
+  const bool timing = flag(e, KTG_FLAG_TIME_SUPPORT);
+  const bool recording = timing || flag(e, KTG_FLAG_COLLECT_WORK);
+  const bool host_loop = flag(e, KTG_FLAG_HOST_LOOP) || e->opt.observer || (e->world > 1) || recording;
   e->work.clear();
   KTG_CUDA(cudaEventRecord(e->ev0, e->stream));
   if (!host_loop) {
@@ -382,16 +388,21 @@ ktg_status run_loop(ktg_engine* e, bool want_sync) {
     KTG_CUDA(cudaMemsetAsync(Sc, 0, (size_t)e->slots * 4, e->stream));
     ktg_round_work w{};
     if (flag(e, KTG_FLAG_COLLECT_WORK)) KTG_TRY(collect_work(e, &w));
-    KTG_TRY(enqueue_round(e, false, 0));
+    KTG_TRY(enqueue_round(e, false, 0, timing ? e->evs0 : nullptr, timing ? e->evs1 : nullptr));
     // removed of this round is hist[round]; read the whole state
     KTG_TRY(read_state(e));
     unsigned long long removed = 0;
     if (round < (uint32_t)kHistCap) {
       KTG_CUDA(cudaMemcpy(&removed, e->d_hist + round, 8, cudaMemcpyDeviceToHost));
     }
-    if (flag(e, KTG_FLAG_COLLECT_WORK)) {
+    if (recording) {
       w.triangles = e->h_st->last_triangles;
       w.removed = removed;
+      if (timing) {
+        float ms = 0;
+        KTG_CUDA(cudaEventElapsedTime(&ms, e->evs0, e->evs1));
+        w.support_ms = ms;
+      }
       e->work.push_back(w);
     }
     if (e->opt.observer) {
@@ -573,6 +584,8 @@ void ktg_engine_destroy(ktg_engine* e) {
   if (e->h_st) cudaFreeHost(e->h_st);
   if (e->ev0) cudaEventDestroy(e->ev0);
   if (e->ev1) cudaEventDestroy(e->ev1);
+  if (e->evs0) cudaEventDestroy(e->evs0);
+  if (e->evs1) cudaEventDestroy(e->evs1);
   if (e->own_stream && e->stream) cudaStreamDestroy(e->stream);
   delete e;
 }

@@ -129,12 +129,14 @@ class _RunInfo(ctypes.Structure):
 
 
 class _RoundWork(ctypes.Structure):
-    _fields_ = [("live_edges", _u64), ("L", _u64), ("triangles", _u64), ("removed", _u64)]
+    _fields_ = [("live_edges", _u64), ("L", _u64), ("triangles", _u64), ("removed", _u64),
+                ("support_ms", ctypes.c_double)]
 
 
 FLAG_HOST_LOOP = 1
 FLAG_NAIVE_SUPPORT = 2
 FLAG_COLLECT_WORK = 4
+FLAG_TIME_SUPPORT = 8
 
 _configured = False
 
@@ -377,12 +379,14 @@ class Engine:
     """A graph resident in HBM with its pristine copy; ktg_engine_* calls."""
 
     def __init__(self, graph: Optional[ZeroTerminatedCsr] = None, options: Optional[TrussOptions] = None,
-                 collect_work: bool = False, stream: Optional[int] = None):
+                 collect_work: bool = False, time_support: bool = False, stream: Optional[int] = None):
         L = lib()
         self._keep = {"graph": graph}
         o = _options(options, self._keep)
         if collect_work:
             o.flags |= FLAG_COLLECT_WORK
+        if time_support:
+            o.flags |= FLAG_TIME_SUPPORT
         if stream is not None:
             o.stream = _vp(stream)
         self._h = _vp()
@@ -423,6 +427,28 @@ class Engine:
         it = _u32()
         _check(lib().ktg_engine_run(self._h, k, _p(hist), cap, ctypes.byref(it)))
         return [int(x) for x in hist[:min(it.value, cap)]]
+
+    def kmax(self) -> int:
+        """kmax_search's search (truss.cpp:73-103) on the resident graph: bound
+        by one support pass, binary search with every probe from pristine.
+        Leaves the engine holding the k_max truss."""
+        self.reset()
+        self.support_pass()
+        max_support = int(self.info()["max_support"])
+        lo = 2
+        if max_support > 0:
+            lo, hi = 3, max_support + 2
+            while lo < hi:
+                mid = lo + (hi - lo + 1) // 2
+                self.reset()
+                self.run(mid)
+                if self.info()["live_edges"] == 0:
+                    hi = mid - 1
+                else:
+                    lo = mid
+        self.reset()
+        self.run(lo)
+        return lo
 
     def support_pass(self) -> int:
         tri = _u64()

@@ -1,0 +1,138 @@
+"""Large-graph parity: byte-exact (col_idx, S, removed history) against the
+oracle at s14 for every K, s20 at K=3 / K_max, plus size-independent
+properties and the pinned known answers of SURVEY §8(d)."""
+import numpy as np
+import pytest
+
+import paper_2009_07929_b200 as kt
+from _util import digest, golden, skew_graph
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.mark.parametrize("scale", [10, 12])
+def test_golden_rmat(scale):
+    ent = golden("rmat.json")[f"s{scale}"]
+    g = kt.rmat(scale)
+    S = kt.SupportArray.zeros(g.total_slots())
+    assert kt.compute_supports(g, S) == ent["triangles"] and digest(S.counts) == ent["supports_sha256"]
+    r = kt.ktruss(g, 3)
+    assert digest(r.edges) == ent["k3_edges_sha256"] and r.removed_per_iteration == ent["k3_removed"]
+    km = kt.kmax_search(g)
+    assert km.k_max == ent["kmax"] and digest(km.truss.edges) == ent["kmax_edges_sha256"]
+
+
+@pytest.fixture(scope="module")
+def s14():
+    return kt.rmat(14)
+
+
+def test_s14_every_k_byte_exact(s14, port):
+    ent = golden("rmat.json")["s14_known"]
+    eng = kt.Engine(s14)
+    for k in range(3, ent["kmax"] + 2):
+        eng.reset()
+        hist = eng.run(k)
+        col, S = eng.read()
+        col_e, S_e, hist_e = port.run_fixpoint(s14, k, threads=8)
+        assert hist == hist_e, k
+        assert np.array_equal(col, col_e) and np.array_equal(S, S_e), k
+        if k == 3:
+            assert eng.info()["live_edges"] == ent["k3_survivors"]
+        if k == ent["kmax"]:
+            assert eng.info()["live_edges"] == ent["kmax_survivors"]
+        if k == ent["kmax"] + 1:
+            assert eng.info()["live_edges"] == 0
+    assert eng.kmax() == ent["kmax"]
+
+
+def test_s14_naive_and_host_loop_agree(s14):
+    base = kt.ktruss(s14, 5)
+    for o in (kt.TrussOptions(naive_support=True), kt.TrussOptions(host_loop=True)):
+        r = kt.ktruss(s14, 5, o)
+        assert np.array_equal(r.edges, base.edges) and r.removed_per_iteration == base.removed_per_iteration
+
+
+def test_incremental_runs_equal_pristine(s14):
+    """Running K+1 on the K-truss (no reset) gives the pristine (K+1)-truss:
+    exercises the device-side buffer parity across runs."""
+    eng = kt.Engine(s14)
+    ref_eng = kt.Engine(s14)
+    eng.reset()
+    for k in range(3, 40, 3):
+        eng.run(k)
+        ref_eng.reset()
+        ref_eng.run(k)
+        a, b = eng.read(), ref_eng.read()
+        assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]), k
+
+
+def test_virtual_gpus_partition_sums_to_full(s14):
+    """Multi-GPU split simulated on one device: the partial
+    supports of P disjoint task shares sum to the full supports."""
+    full = kt.Engine(s14)
+    full.reset()
+    t_full = full.support_pass()
+    S_full = full.read()[1]
+    for P in (2, 3, 8):
+        acc = np.zeros_like(S_full, dtype=np.uint64)
+        tri = 0
+        for r in range(P):
+            e = kt.Engine(s14)
+            e.set_partition(r, P, allreduce=lambda *a: 0)
+            e.reset()
+            tri += e.support_pass()
+            acc += e.read()[1]
+        assert tri == t_full and np.array_equal(acc.astype(np.uint32), S_full), P
+
+
+def test_skew_graph(port):
+    g = skew_graph()
+    for k in (3, 4):
+        r = kt.ktruss(g, k)
+        e, hist = port.truss_edges(g, k, threads=8)
+        assert np.array_equal(r.edges, e) and r.removed_per_iteration == hist
+
+
+def test_er_small(port):
+    g = kt.erdos_renyi(16, 16 << 16, 42)
+    for k in (3, 4):
+        r = kt.ktruss(g, k)
+        e, hist = port.truss_edges(g, k, threads=8)
+        assert np.array_equal(r.edges, e) and r.removed_per_iteration == hist
+    assert kt.kmax_search(g).k_max == port.kmax(g, threads=8)
+
+
+@pytest.fixture(scope="module")
+def s20():
+    return kt.rmat(20)
+
+
+def test_s20_known_answers_and_properties(s20):
+    ent = golden("rmat.json")["s20_known"]
+    assert (s20.num_vertices, s20.num_edges) == (ent["n"], ent["m"])
+    eng = kt.Engine(s20)
+    eng.reset()
+    t = eng.support_pass()
+    col, S = eng.read()
+    assert t == ent["triangles"] and int(S.max()) == ent["max_support"]
+    assert int(S.sum(dtype=np.uint64)) == 3 * t  # triple-count identity
+    eng.reset()
+    eng.run(3)
+    assert eng.info()["live_edges"] == ent["k3_survivors"]
+    # idempotence: the truss is a fixpoint of its own k
+    hist = eng.run(3)
+    assert hist == [0]
+    assert eng.kmax() == ent["kmax"]
+    assert eng.info()["live_edges"] == ent["kmax_survivors"]
+
+
+@pytest.mark.parametrize("k", [3, 304])
+def test_s20_byte_exact(s20, port, k):
+    eng = kt.Engine(s20)
+    eng.reset()
+    hist = eng.run(k)
+    col, S = eng.read()
+    col_e, S_e, hist_e = port.run_fixpoint(s20, k, threads=16)
+    assert hist == hist_e
+    assert np.array_equal(col, col_e) and np.array_equal(S, S_e)
