@@ -68,6 +68,9 @@ struct ktg_engine {
   uint32_t nchunks = 0;
   uint64_t live_pristine = 0;
   bool has_graph = false;
+  bool pristine_valid = false;
+  size_t cap_row_ptr = 0, cap_col = 0, cap_colp = 0, cap_S0 = 0, cap_S1 = 0, cap_deg = 0, cap_degp = 0,
+         cap_chunk_row = 0, cap_pair_counts = 0, cap_heavy = 0, cap_pairs = 0;
 
   uint32_t* d_row_ptr = nullptr;
   uint32_t* d_col = nullptr;
@@ -93,6 +96,9 @@ struct ktg_engine {
 
   cudaGraphExec_t exec = nullptr;
   int exec_naive = -1, exec_w16 = -1;
+  uint64_t exec_slots = 0;
+  uint32_t exec_n = 0;
+  const void* exec_col = nullptr;
 
   uint32_t rank = 0, world = 1;
   ktg_allreduce_cb allreduce = nullptr;
@@ -126,6 +132,8 @@ struct ktg_engine {
   void free_graph() {
     if (exec) cudaGraphExecDestroy(exec);
     exec = nullptr;
+    cap_row_ptr = cap_col = cap_colp = cap_S0 = cap_S1 = cap_deg = cap_degp = cap_chunk_row = 0;
+    cap_pair_counts = cap_heavy = cap_pairs = 0;
     dfree(d_row_ptr);
     dfree(d_col);
     dfree(d_col_pristine);
@@ -199,58 +207,73 @@ ktg_status engine_init(const ktg_options* opt, ktg_engine* e) {
   return KTG_OK;
 }
 
+ktg_status read_state(ktg_engine* e) {
+  KTG_CUDA(cudaMemcpyAsync(e->h_st, e->d_st, sizeof(DevState), cudaMemcpyDeviceToHost, e->stream));
+  KTG_CUDA(cudaStreamSynchronize(e->stream));
+  return KTG_OK;
+}
+
+template <typename T>
+ktg_status ensure(T*& p, size_t& cap, size_t bytes) {
+  if (p && cap >= bytes) return KTG_OK;
+  if (p) cudaFree(p);
+  p = nullptr;
+  cap = 0;
+  KTG_CUDA(cudaMalloc(&p, bytes));
+  cap = bytes;
+  return KTG_OK;
+}
+
 // Uploads (host or device source) and prepares the per-graph structures.
+// Device buffers are reused when the new graph fits (the host-buffer entry
+// points keep one cached engine per thread, so repeated calls do no
+// allocation and reuse the instantiated CUDA graph).
 ktg_status engine_load(ktg_engine* e, const uint32_t* row_ptr, uint32_t n, const uint32_t* col,
                        uint64_t slots, cudaMemcpyKind kind, bool keep_pristine) {
   if (n == 0) return fail(KTG_ERR_INVALID_INPUT, "csr has no vertices");
   if (slots > 0xFFFFFFFFull) return fail(KTG_ERR_INVALID_INPUT, "slot count exceeds 32-bit offsets");
   if (slots < n) return fail(KTG_ERR_INVALID_INPUT, "row_ptr end does not match slot count");
-  e->free_graph();
+  e->has_graph = false;
   e->n = n;
   e->slots = slots;
   e->nchunks = (uint32_t)((slots + kChunk - 1) / kChunk);
   const size_t nb = (size_t)(n + 2) * 4;
   const size_t sb = (size_t)slots * 4 + 16;  // +16: vector-load padding
-  KTG_CUDA(cudaMalloc(&e->d_row_ptr, nb));
-  KTG_CUDA(cudaMalloc(&e->d_col, sb));
-  KTG_CUDA(cudaMalloc(&e->d_S0, sb));
-  KTG_CUDA(cudaMalloc(&e->d_S1, sb));
-  KTG_CUDA(cudaMalloc(&e->d_deg, nb));
-  KTG_CUDA(cudaMalloc(&e->d_deg_pristine, nb));
-  KTG_CUDA(cudaMalloc(&e->d_chunk_row, (size_t)e->nchunks * 4));
-  KTG_CUDA(cudaMalloc(&e->d_pair_counts, (size_t)e->nchunks * 4));
-  KTG_CUDA(cudaMalloc(&e->d_heavy, nb));
+  KTG_TRY(ensure(e->d_row_ptr, e->cap_row_ptr, nb));
+  KTG_TRY(ensure(e->d_col, e->cap_col, sb));
+  KTG_TRY(ensure(e->d_S0, e->cap_S0, sb));
+  KTG_TRY(ensure(e->d_S1, e->cap_S1, sb));
+  KTG_TRY(ensure(e->d_deg, e->cap_deg, nb));
+  KTG_TRY(ensure(e->d_deg_pristine, e->cap_degp, nb));
+  KTG_TRY(ensure(e->d_chunk_row, e->cap_chunk_row, (size_t)e->nchunks * 4));
+  KTG_TRY(ensure(e->d_pair_counts, e->cap_pair_counts, (size_t)e->nchunks * 4));
+  KTG_TRY(ensure(e->d_heavy, e->cap_heavy, nb));
   KTG_CUDA(cudaMemcpyAsync(e->d_row_ptr, row_ptr, nb, kind, e->stream));
   KTG_CUDA(cudaMemcpyAsync(e->d_col, col, (size_t)slots * 4, kind, e->stream));
   KTG_CUDA(cudaMemsetAsync(e->d_col + slots, 0, 16, e->stream));
+  e->pristine_valid = false;
   if (keep_pristine) {
-    KTG_CUDA(cudaMalloc(&e->d_col_pristine, sb));
+    KTG_TRY(ensure(e->d_col_pristine, e->cap_colp, sb));
     KTG_CUDA(cudaMemcpyAsync(e->d_col_pristine, e->d_col, sb, cudaMemcpyDeviceToDevice, e->stream));
+    e->pristine_valid = true;
   }
   KTG_CUDA(cudaMemsetAsync(e->d_S0, 0, sb, e->stream));
   KTG_CUDA(cudaMemsetAsync(e->d_S1, 0, sb, e->stream));
   KTG_CUDA(cudaMemsetAsync(e->d_deg, 0, nb, e->stream));
-  KTG_CUDA(cudaMemsetAsync(&e->d_st->live, 0, sizeof(unsigned long long), e->stream));
-  k_init_deg<<<e->prune_grid, kPruneThreads, 0, e->stream>>>(e->d_row_ptr, e->d_col, n, e->d_deg, e->d_st);
+  KTG_CUDA(cudaMemsetAsync(e->d_st, 0, sizeof(DevState), e->stream));
+  k_init_deg<<<4 * e->num_sms, 256, 0, e->stream>>>(e->d_row_ptr, e->d_col, n, slots, e->d_deg, e->d_st);
   KTG_CUDA(cudaGetLastError());
   k_chunk_rows<<<(e->nchunks + 255) / 256, 256, 0, e->stream>>>(e->d_row_ptr, n, slots, e->nchunks,
                                                                e->d_chunk_row);
   KTG_CUDA(cudaGetLastError());
   KTG_CUDA(cudaMemcpyAsync(e->d_deg_pristine, e->d_deg, nb, cudaMemcpyDeviceToDevice, e->stream));
   // Off-diagonal task capacity: the pristine plan is the largest (live ends
-  // only shrink as rows are pruned).
+  // only shrink as rows are pruned); k_plan_count totals it on the device.
   Graph g = e->dev_graph();
-  k_plan_count<<<(e->nchunks + 255) / 256, 256, 0, e->stream>>>(g);
+  k_plan_count<<<(e->nchunks + 255) / 256, 256, 0, e->stream>>>(g, 1);
   KTG_CUDA(cudaGetLastError());
-  std::vector<uint32_t> counts(e->nchunks);
-  KTG_CUDA(cudaMemcpyAsync(counts.data(), e->d_pair_counts, (size_t)e->nchunks * 4, cudaMemcpyDeviceToHost,
-                           e->stream));
-  KTG_CUDA(cudaMemcpyAsync(&e->h_st->live, &e->d_st->live, sizeof(unsigned long long),
-                           cudaMemcpyDeviceToHost, e->stream));
-  KTG_CUDA(cudaStreamSynchronize(e->stream));
-  uint64_t npairs = 0;
-  for (uint32_t c : counts) npairs += c;
-  KTG_CUDA(cudaMalloc(&e->d_pairs, sizeof(uint2) * std::max<uint64_t>(1, npairs)));
+  KTG_TRY(read_state(e));
+  KTG_TRY(ensure(e->d_pairs, e->cap_pairs, sizeof(uint2) * std::max<uint64_t>(1, e->h_st->pairs_needed)));
   e->live_pristine = e->h_st->live;
   e->has_graph = true;
   return KTG_OK;
@@ -262,7 +285,7 @@ ktg_status enqueue_round(ktg_engine* e, bool graph_mode, cudaGraphConditionalHan
   Graph g = e->dev_graph();
   const cudaStream_t s = e->stream;
   const int fused = graph_mode ? 1 : 0;
-  k_plan_count<<<(e->nchunks + 255) / 256, 256, 0, s>>>(g);
+  k_plan_count<<<(e->nchunks + 255) / 256, 256, 0, s>>>(g, 0);
   k_plan_write<<<1, 1024, 0, s>>>(g);
   if (sup0) KTG_CUDA(cudaEventRecord(sup0, s));
   if (flag(e, KTG_FLAG_NAIVE_SUPPORT)) {
@@ -290,7 +313,9 @@ ktg_status enqueue_round(ktg_engine* e, bool graph_mode, cudaGraphConditionalHan
 ktg_status build_graph(ktg_engine* e) {
   const int naive = flag(e, KTG_FLAG_NAIVE_SUPPORT) ? 1 : 0;
   const int w16 = e->opt.width_bits == 16 ? 1 : 0;
-  if (e->exec && e->exec_naive == naive && e->exec_w16 == w16) return KTG_OK;
+  if (e->exec && e->exec_naive == naive && e->exec_w16 == w16 && e->exec_n == e->n &&
+      e->exec_slots == e->slots && e->exec_col == e->d_col)
+    return KTG_OK;
   if (e->exec) cudaGraphExecDestroy(e->exec);
   e->exec = nullptr;
   cudaGraph_t graph;
@@ -324,6 +349,9 @@ ktg_status build_graph(ktg_engine* e) {
   if (ie != cudaSuccess) return fail(KTG_ERR_CUDA, std::string("cudaGraphInstantiate: ") + cudaGetErrorString(ie));
   e->exec_naive = naive;
   e->exec_w16 = w16;
+  e->exec_n = e->n;
+  e->exec_slots = e->slots;
+  e->exec_col = e->d_col;
   return KTG_OK;
 }
 
@@ -335,12 +363,6 @@ __global__ void k_set_live(DevState* st, unsigned long long live) { st->live = l
 ktg_status begin_run(ktg_engine* e, uint32_t k, int parity) {
   k_begin<<<1, 1, 0, e->stream>>>(e->d_st, k >= 2 ? k - 2 : 0, e->opt.width_bits == 16 ? 1 : 0, parity);
   KTG_CUDA(cudaGetLastError());
-  return KTG_OK;
-}
-
-ktg_status read_state(ktg_engine* e) {
-  KTG_CUDA(cudaMemcpyAsync(e->h_st, e->d_st, sizeof(DevState), cudaMemcpyDeviceToHost, e->stream));
-  KTG_CUDA(cudaStreamSynchronize(e->stream));
   return KTG_OK;
 }
 
@@ -449,7 +471,7 @@ ktg_status copy_hist(ktg_engine* e, uint64_t* hist, uint32_t cap, uint32_t* iter
 ktg_status support_pass(ktg_engine* e, int parity, uint64_t* triangles, bool max_support) {
   Graph g = e->dev_graph();
   k_begin<<<1, 1, 0, e->stream>>>(e->d_st, 0, e->opt.width_bits == 16 ? 1 : 0, parity);
-  k_plan_count<<<(e->nchunks + 255) / 256, 256, 0, e->stream>>>(g);
+  k_plan_count<<<(e->nchunks + 255) / 256, 256, 0, e->stream>>>(g, 0);
   k_plan_write<<<1, 1024, 0, e->stream>>>(g);
   if (flag(e, KTG_FLAG_NAIVE_SUPPORT))
     k_support_naive<<<4 * e->num_sms, 256, 0, e->stream>>>(g);
@@ -509,7 +531,7 @@ ktg_status extract(ktg_engine* e, uint32_t* u, uint32_t* v, uint32_t* s, uint64_
 
 ktg_status reset(ktg_engine* e) {
   if (!e->has_graph) return fail(KTG_ERR_INVALID_PARAMETER, "engine has no graph loaded");
-  if (!e->d_col_pristine) return fail(KTG_ERR_INVALID_PARAMETER, "engine was loaded without a pristine copy");
+  if (!e->pristine_valid) return fail(KTG_ERR_INVALID_PARAMETER, "engine was loaded without a pristine copy");
   const size_t sb = (size_t)e->slots * 4;
   KTG_CUDA(cudaMemcpyAsync(e->d_col, e->d_col_pristine, sb, cudaMemcpyDeviceToDevice, e->stream));
   KTG_CUDA(cudaMemcpyAsync(e->d_deg, e->d_deg_pristine, (size_t)(e->n + 2) * 4, cudaMemcpyDeviceToDevice,
@@ -521,15 +543,59 @@ ktg_status reset(ktg_engine* e) {
   return KTG_OK;
 }
 
-// RAII temporary engine for the host-pointer entry points.
+// Engine for the host-pointer entry points: one cached engine per thread
+// and device (buffers and the instantiated fixpoint graph are reused across
+// calls); a caller-supplied stream gets a private engine.
 struct TmpEngine {
   ktg_engine* e = nullptr;
-  ~TmpEngine() { ktg_engine_destroy(e); }
+  bool owned = false;
+  ~TmpEngine() {
+    if (owned) ktg_engine_destroy(e);
+  }
 };
+
+thread_local ktg_engine* t_cached[64] = {};
 
 ktg_status tmp_engine(const ktg_options* opt, const uint32_t* row_ptr, uint32_t n, const uint32_t* col,
                       uint64_t slots, bool pristine, TmpEngine& t) {
-  KTG_TRY(ktg_engine_create(opt, &t.e));
+  ktg_options o;
+  if (opt) {
+    if (opt->struct_size != sizeof(ktg_options))
+      return fail(KTG_ERR_INVALID_PARAMETER, "ktg_options.struct_size mismatch");
+    o = *opt;
+  } else {
+    ktg_options_init(&o);
+  }
+  if (o.width_bits != 32 && o.width_bits != 16) return fail(KTG_ERR_INVALID_PARAMETER, "width_bits must be 16 or 32");
+  int dev = o.device;
+  if (dev < 0) {
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
+      cudaGetLastError();
+      return fail(KTG_ERR_NO_DEVICE, "no CUDA device visible (the engine has no CPU fallback)");
+    }
+    KTG_CUDA(cudaGetDevice(&dev));
+  }
+  if (o.stream == nullptr && dev >= 0 && dev < 64) {
+    if (!t_cached[dev]) {
+      ktg_options base = o;
+      base.flags = 0;
+      base.observer = nullptr;
+      base.device = dev;
+      KTG_TRY(ktg_engine_create(&base, &t_cached[dev]));
+    }
+    t.e = t_cached[dev];
+    t.owned = false;
+    KTG_CUDA(cudaSetDevice(dev));
+    const cudaStream_t keep = t.e->stream;
+    t.e->opt = o;
+    t.e->opt.device = dev;
+    t.e->opt.stream = nullptr;
+    t.e->stream = keep;
+  } else {
+    KTG_TRY(ktg_engine_create(&o, &t.e));
+    t.owned = true;
+  }
   return engine_load(t.e, row_ptr, n, col, slots, cudaMemcpyHostToDevice, pristine);
 }
 

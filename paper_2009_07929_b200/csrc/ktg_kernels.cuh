@@ -43,6 +43,7 @@ struct DevState {
   unsigned int max_support;          // max S seen by k_max_support
   unsigned int width16;              // check supports against 65535
   unsigned int pad;
+  unsigned long long pairs_needed;   // off-diagonal task capacity (load time)
 };
 
 struct Graph {
@@ -90,33 +91,30 @@ __device__ __forceinline__ uint32_t upper_bound_g(const uint32_t* __restrict__ a
 // Setup kernels
 // ---------------------------------------------------------------------------
 
-// Live out-degree of every row (position of the first zero; rows are
-// zero-prefix-free, csr.hpp:12-16) and the live total. Warp per row.
+// Live out-degree of every row and the live total, slot-parallel: the last
+// live slot of a row is a nonzero followed by a zero (rows are zero-prefix-
+// free and end in a zero, csr.hpp:12-16), so each row is found once with a
+// binary search over row_ptr. deg must be zeroed (rows with no live slot).
 __global__ void k_init_deg(const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ col,
-                           uint32_t n, uint32_t* __restrict__ deg, DevState* st) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+                           uint32_t n, uint64_t slots, uint32_t* __restrict__ deg, DevState* st) {
   unsigned long long live = 0;
-  for (uint32_t v = warp + 1; v <= n; v += nwarps) {
-    const uint32_t b = row_ptr[v], e = row_ptr[v + 1];
-    uint32_t d = e - b;  // if no zero found (invalid CSR) fall back to the span
-    for (uint32_t off = b; off < e; off += 32) {
-      const uint32_t x = off + lane;
-      const bool z = x < e && col[x] == 0;
-      const unsigned m = __ballot_sync(0xffffffffu, z);
-      if (m) {
-        d = off + __ffs(m) - 1 - b;
-        break;
+  for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s + 1 < slots;
+       s += (uint64_t)gridDim.x * blockDim.x) {
+    if (col[s] != 0 && col[s + 1] == 0) {
+      uint32_t lo = 0, hi = n + 2;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (row_ptr[mid] <= (uint32_t)s) lo = mid + 1; else hi = mid;
       }
-    }
-    if (lane == 0) {
-      deg[v] = d;
+      const uint32_t row = lo - 1;
+      const uint32_t d = (uint32_t)s - row_ptr[row] + 1;
+      deg[row] = d;
       live += d;
     }
   }
-  if (lane == 0 && live) atomicAdd(&st->live, live);
-  if (blockIdx.x == 0 && threadIdx.x == 0) deg[0] = 0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) live += __shfl_xor_sync(0xffffffffu, live, o);
+  if ((threadIdx.x & 31) == 0 && live) atomicAdd(&st->live, live);
 }
 
 // Row containing the last slot of every chunk (fixed for the graph's life).
@@ -144,7 +142,7 @@ __global__ void k_chunk_rows(const uint32_t* __restrict__ row_ptr, uint32_t n, u
 // extend past it, and its pivots get one off-diagonal task per further chunk
 // its live part reaches.
 
-__global__ void k_plan_count(Graph g) {
+__global__ void k_plan_count(Graph g, int total) {
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= g.nchunks) return;
   const uint32_t i = g.chunk_row[q];
@@ -155,6 +153,7 @@ __global__ void k_plan_count(Graph g) {
     if (le > e) cnt = (uint32_t)((le - 1) / kChunk - q);
   }
   g.pair_counts[q] = cnt;
+  if (total && cnt) atomicAdd(&g.st->pairs_needed, (unsigned long long)cnt);
 }
 
 // Single CTA: exclusive scan of pair_counts, write the pair list, reset the
