@@ -69,8 +69,11 @@ enum {
                                        Listing 1), for cross-checking only    */
   KTG_FLAG_COLLECT_WORK = 1u << 2,  /* record per-round closed-form work L_r,
                                        live edges and triangles (extra kernels) */
-  KTG_FLAG_TIME_SUPPORT = 1u << 3   /* host loop; CUDA events around every
+  KTG_FLAG_TIME_SUPPORT = 1u << 3,  /* host loop; CUDA events around every
                                        support launch (ktg_round_work.support_ms) */
+  KTG_FLAG_LABEL_ORDER = 1u << 4    /* run the fixpoint on the caller's (label-
+                                       ordered) CSR instead of the internal
+                                       degree-ordered working copy */
 };
 
 typedef struct {

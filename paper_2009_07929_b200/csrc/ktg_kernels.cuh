@@ -63,6 +63,8 @@ struct Graph {
   uint64_t slots;
   uint32_t rank;            // multi-GPU task split
   uint32_t world;
+  uint32_t scan_ratio;      // SCAN N+(j) when |N+(j)| <= ratio * |tail|
+  uint32_t* payload;        // per-slot id compacted along with col (working layout) or null
 };
 
 __host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
@@ -200,23 +202,51 @@ __global__ void __launch_bounds__(1024) k_plan_write(Graph g) {
 // ---------------------------------------------------------------------------
 // Support kernel
 // ---------------------------------------------------------------------------
+constexpr int kFilterBits = 1 << 15;     // membership filter over (value, row run)
+constexpr int kStrip = 256;              // flat elements a warp takes per grab (8 per lane)
+constexpr int kQueue = 64;               // per-warp queue of filter positives
+
 struct SupportSmem {
-  uint32_t A[kChunk];        // staged slots col[a0 .. a0+alen)
-  uint32_t cntA[kChunk];     // pending increments of staged slots
-  uint32_t cntP[kChunk];     // pending pivot counts (off-diagonal tasks)
-  uint32_t pref[kChunk + 1]; // exclusive prefix of per-pivot cost
-  uint32_t b0[kChunk];       // clipped N+(j) range [b0, b1)
+  uint32_t A[kChunk];          // staged slots col[a0 .. a0+alen)
+  uint32_t cntA[kChunk];       // pending increments of staged slots
+  union {
+    uint16_t nz[2 * kChunk];   // prologue: next zero at or after x (alen if none)
+    uint32_t cntP[kChunk];     // work loop: pending pivot counts (off-diagonal)
+  };
+  uint32_t pref[kChunk + 1];   // exclusive prefix of per-pivot cost
+  uint32_t b0[kChunk];         // clipped N+(j) range [b0, b1)
   uint32_t b1[kChunk];
-  uint16_t nz[kChunk];       // next zero at or after x (alen if none)
-  uint16_t tb[kChunk];       // tail range [tb, te) relative to a0
-  uint16_t te[kChunk];
-  uint8_t mode[kChunk];      // 1 = scan N+(j), 0 = iterate the tail
+  uint16_t te[kChunk];         // tail end (relative to a0) | 0x8000 if SCAN mode
+  uint32_t filt[kFilterBits / 32];
+  uint32_t qk[kSupportThreads / 32][kQueue];   // queued (value, col position, pivot)
+  uint32_t qpos[kSupportThreads / 32][kQueue];
+  uint16_t qp[kSupportThreads / 32][kQueue];
   uint32_t red[kSupportThreads / 32];
   uint32_t task;
+  uint32_t next;               // flat work counter of the current task
 };
 
+__device__ __forceinline__ uint32_t filt_hash(uint32_t k, uint32_t te) {
+  return ((k ^ (te * 0x85EBCA6Bu)) * 2654435761u) >> (32 - 15);
+}
+
+// lower_bound in smem A[lo, hi)
+__device__ __forceinline__ uint32_t lower_bound_s(const uint32_t* A, uint32_t lo, uint32_t hi, uint32_t key) {
+  uint32_t len = hi - lo;
+  while (len > 0) {
+    const uint32_t half = len >> 1;
+    if (A[lo + half] < key) {
+      lo += half + 1;
+      len -= half + 1;
+    } else {
+      len = half;
+    }
+  }
+  return lo;
+}
+
 // Block-wide exclusive scan of one u32 per thread; returns the prefix, total
-// in *total. Uses s.red as scratch.
+// in *total. Uses red as scratch.
 __device__ __forceinline__ uint32_t block_exscan(uint32_t v, uint32_t* red, uint32_t* total) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   constexpr int NW = kSupportThreads / 32;
@@ -244,14 +274,34 @@ __device__ __forceinline__ uint32_t block_exscan(uint32_t v, uint32_t* red, uint
   return r;
 }
 
+// Confirms one queued filter positive: binary search of k in the pivot's
+// tail; on a match bumps the tail slot (smem), the A22 slot (global) and the
+// pivot count (smem).
+__device__ __forceinline__ bool confirm(SupportSmem& s, uint32_t* __restrict__ S, uint32_t* cntPiv, bool diag,
+                                        uint32_t k, uint32_t pos, uint32_t p) {
+  const uint32_t te = s.te[p] & 0x7fffu;
+  const uint32_t tb = diag ? p + 1 : 0;
+  const uint32_t x = lower_bound_s(s.A, tb, te, k);
+  if (x < te && s.A[x] == k) {
+    atomicAdd(&s.cntA[x], 1u);
+    atomicAdd(&S[pos], 1u);
+    atomicAdd(&cntPiv[p], 1u);
+    return true;
+  }
+  return false;
+}
+
 // Persistent CTAs pull tasks (q, q2) off a counter. Per task:
-//   1. stage chunk q2 of col in smem, find the next zero of every position;
+//   1. stage chunk q2 of col in smem, find the next zero of every position,
+//      set a membership-filter bit for every (value, row-run end) pair;
 //   2. per pivot slot s=(i,j) in chunk q: its a12 tail within the staged chunk
-//      [tb, te); clip N+(j) to the tail's value range; choose SCAN (read
-//      N+(j) coalesced, binary-search each element in the smem tail) or
+//      [tb, te); clip N+(j) to the tail's value range; choose SCAN (read the
+//      clipped N+(j) coalesced and test each element against the filter) or
 //      ITERATE (binary-search each tail element in N+(j)) by cost;
-//   3. flatten all pivots' work with a prefix sum and split it evenly over
-//      the warps; each lane does one element per step;
+//   3. flatten all pivots' work with a prefix sum; warps grab strips of it
+//      dynamically; each lane caches its pivot's descriptor in registers;
+//      SCAN elements that pass the filter (~hits + 1.5% false positives) are
+//      queued per warp and confirmed 32 at a time by a full-warp binary search;
 //   4. a match (i,j,k) adds 1 to S[slot(i,k)] (smem), S[slot(j,k)] (global
 //      red.add) and the pivot's count (smem); smem counts are flushed once.
 // Semantically each pivot slot gets exactly intersect_tails' matches
@@ -264,14 +314,22 @@ k_support_chunked(Graph g) {
   const int lane = tid & 31, wid = tid >> 5;
   constexpr int NW = kSupportThreads / 32;
   constexpr int EPT = kChunk / kSupportThreads;
+  constexpr int FPT = kFilterBits / 32 / kSupportThreads;
   uint32_t* __restrict__ S = cur_S(g);
   const uint32_t* __restrict__ col = g.col;
   const uint32_t npairs = g.st->npairs;
   const uint32_t ntasks = npairs + g.nchunks;
+  const uint32_t ratio = g.scan_ratio;
+  const unsigned lt_mask = (1u << lane) - 1u;
   unsigned long long tri_local = 0;
 
   for (;;) {
-    if (tid == 0) s.task = atomicAdd(&g.st->task_next, 1u);
+    if (tid == 0) {
+      s.task = atomicAdd(&g.st->task_next, 1u);
+      s.next = 0;
+    }
+#pragma unroll
+    for (int e = 0; e < FPT; ++e) s.filt[tid * FPT + e] = 0;
     __syncthreads();
     const uint32_t local = s.task;
     const uint64_t t64 = (uint64_t)local * g.world + g.rank;
@@ -304,10 +362,9 @@ k_support_chunked(Graph g) {
       const uint32_t v = x < alen ? col[a0 + x] : 0u;
       s.A[x] = v;
       s.cntA[x] = 0;
-      s.cntP[x] = 0;
       if (v == 0 && x < alen && first_zero == 0xffffffffu) first_zero = x;
     }
-    // next-zero: exclusive suffix-min of first_zero over higher threads
+    // next-zero: exclusive suffix-min of first_zero over higher threads; filter bits
     {
       uint32_t m = first_zero;
 #pragma unroll
@@ -315,7 +372,6 @@ k_support_chunked(Graph g) {
         const uint32_t y = __shfl_down_sync(0xffffffffu, m, o);
         if (lane + o < 32) m = min(m, y);
       }
-      // m = min over lanes >= lane (inclusive) within warp
       if (lane == 0) s.red[wid] = m;
       __syncthreads();
       uint32_t carry = 0xffffffffu;
@@ -326,8 +382,13 @@ k_support_chunked(Graph g) {
 #pragma unroll
       for (int e = EPT - 1; e >= 0; --e) {
         const uint32_t x = tid * EPT + e;
-        if (x < alen && s.A[x] == 0) cur = x;
+        const uint32_t v = s.A[x];
+        if (x < alen && v == 0) cur = x;
         s.nz[x] = (uint16_t)min(cur, (uint32_t)kChunk);
+        if (v != 0) {
+          const uint32_t h = filt_hash(v, cur);
+          atomicOr(&s.filt[h >> 5], 1u << (h & 31));
+        }
       }
     }
     __syncthreads();
@@ -355,13 +416,11 @@ k_support_chunked(Graph g) {
               const uint32_t blen = b1_ - b0_;
               if (blen) {
                 const uint32_t tlen = te_ - tb_;
-                const bool scan = blen <= tlen * kScanRatio;
+                const bool scan = blen <= tlen * ratio;
                 c = scan ? blen : tlen;
                 s.b0[x] = b0_;
                 s.b1[x] = b1_;
-                s.tb[x] = (uint16_t)tb_;
-                s.te[x] = (uint16_t)te_;
-                s.mode[x] = scan;
+                s.te[x] = (uint16_t)(te_ | (scan ? 0x8000u : 0u));
               }
             }
           }
@@ -381,58 +440,91 @@ k_support_chunked(Graph g) {
     }
     if (tid == 0) s.pref[kChunk] = W;
     __syncthreads();
+    if (!diag) {  // cntP aliases nz, which is dead from here on
+#pragma unroll
+      for (int e = 0; e < EPT; ++e) s.cntP[tid * EPT + e] = 0;
+      __syncthreads();
+    }
 
-    // 3. flattened element work, contiguous range per warp
-    if (W) {
-      const uint32_t beg = (uint32_t)(((uint64_t)W * wid) / NW);
-      const uint32_t end = (uint32_t)(((uint64_t)W * (wid + 1)) / NW);
-      uint32_t f = beg + lane;
-      // first pivot with pref[p+1] > f
+    // 3. flattened element work, strips grabbed dynamically by warps
+    uint32_t* __restrict__ cntPiv = diag ? s.cntA : s.cntP;
+    uint32_t* qk = s.qk[wid];
+    uint32_t* qpos = s.qpos[wid];
+    uint16_t* qp = s.qp[wid];
+    uint32_t qn = 0;
+    for (;;) {
+      uint32_t base = 0;
+      if (lane == 0) base = atomicAdd(&s.next, (uint32_t)kStrip);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (base >= W) break;
+      const uint32_t lim = min(base + (uint32_t)kStrip, W);
       uint32_t p;
       {
         uint32_t lo = 0, hi = kChunk;
-        const uint32_t key = min(f, W - 1);
         while (lo < hi) {
           const uint32_t mid = (lo + hi) >> 1;
-          if (s.pref[mid + 1] <= key) lo = mid + 1; else hi = mid;
+          if (s.pref[mid + 1] <= base) lo = mid + 1; else hi = mid;
         }
         p = lo;
       }
-      for (; f < end; f += 32) {
-        while (s.pref[p + 1] <= f) ++p;
-        const uint32_t o = f - s.pref[p];
-        bool hit = false;
-        if (s.mode[p]) {
-          const uint32_t pos = s.b0[p] + o;
-          const uint32_t k = col[pos];
-          uint32_t lo = s.tb[p], hi = s.te[p];
-          const uint32_t tend = hi;
-          while (lo < hi) {
-            const uint32_t mid = (lo + hi) >> 1;
-            if (s.A[mid] < k) lo = mid + 1; else hi = mid;
+      uint32_t pe = s.pref[p + 1], pb = s.pref[p];
+      uint32_t db0 = s.b0[p], db1 = s.b1[p], dte = s.te[p];
+      bool dscan = dte & 0x8000u;
+      dte &= 0x7fffu;
+      for (uint32_t f0 = base; f0 < lim; f0 += 32) {
+        const uint32_t f = f0 + lane;
+        bool pos_flag = false;
+        uint32_t k = 0, pos = 0;
+        if (f < lim) {
+          if (f >= pe) {
+            do {
+              ++p;
+              pe = s.pref[p + 1];
+            } while (pe <= f);
+            pb = s.pref[p];
+            db0 = s.b0[p];
+            db1 = s.b1[p];
+            dte = s.te[p];
+            dscan = dte & 0x8000u;
+            dte &= 0x7fffu;
           }
-          if (lo < tend && s.A[lo] == k) {
-            atomicAdd(&s.cntA[lo], 1u);
-            atomicAdd(&S[pos], 1u);
-            hit = true;
-          }
-        } else {
-          const uint32_t x = s.tb[p] + o;
-          const uint32_t k = s.A[x];
-          const uint32_t bend = s.b1[p];
-          const uint32_t y = lower_bound_g(col, s.b0[p], bend, k);
-          if (y < bend && __ldg(col + y) == k) {
-            atomicAdd(&s.cntA[x], 1u);
-            atomicAdd(&S[y], 1u);
-            hit = true;
+          const uint32_t o = f - pb;
+          if (dscan) {
+            pos = db0 + o;
+            k = col[pos];
+            const uint32_t h = filt_hash(k, dte);
+            pos_flag = (s.filt[h >> 5] >> (h & 31)) & 1u;
+          } else {
+            const uint32_t x = (diag ? p + 1 : 0) + o;
+            const uint32_t kk = s.A[x];
+            const uint32_t y = lower_bound_g(col, db0, db1, kk);
+            if (y < db1 && __ldg(col + y) == kk) {
+              atomicAdd(&s.cntA[x], 1u);
+              atomicAdd(&S[y], 1u);
+              atomicAdd(&cntPiv[p], 1u);
+              ++tri_local;
+            }
           }
         }
-        if (hit) {
-          ++tri_local;
-          atomicAdd(diag ? &s.cntA[p] : &s.cntP[p], 1u);
+        const unsigned m = __ballot_sync(0xffffffffu, pos_flag);
+        if (pos_flag) {
+          const uint32_t slot = qn + __popc(m & lt_mask);
+          qk[slot] = k;
+          qpos[slot] = pos;
+          qp[slot] = (uint16_t)p;
+        }
+        qn += __popc(m);
+        if (qn >= 32) {
+          __syncwarp();
+          const uint32_t e = qn - 32 + lane;
+          tri_local += confirm(s, S, cntPiv, diag, qk[e], qpos[e], qp[e]);
+          qn -= 32;
+          __syncwarp();
         }
       }
     }
+    __syncwarp();
+    if (lane < qn) tri_local += confirm(s, S, cntPiv, diag, qk[lane], qpos[lane], qp[lane]);
     __syncthreads();
 
     // 4. flush smem counts
@@ -510,13 +602,17 @@ __global__ void k_intersect_one(const uint32_t* __restrict__ row_ptr, const uint
   *found = f;
 }
 
-// First slot whose support exceeds 65535 (check_16bit, support.cpp:53-60).
+// First slot whose support exceeds 65535 (check_16bit, support.cpp:53-60),
+// in the CALLER's slot numbering (payload maps working slots back), packed
+// as slot << 32 | count so one atomicMin keeps the reference's first slot.
 __global__ void k_check16(Graph g) {
   const uint32_t* __restrict__ S = cur_S(g);
   for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < g.slots;
        x += (uint64_t)gridDim.x * blockDim.x) {
-    if (S[x] > 0xFFFFu) {
-      atomicMin(&g.st->overflow_slot, (unsigned long long)x);
+    const uint32_t v = S[x];
+    if (v > 0xFFFFu) {
+      const unsigned long long slot = g.payload ? g.payload[x] : x;
+      atomicMin(&g.st->overflow_slot, (slot << 32) | v);
       g.st->error = 1;
     }
   }
@@ -544,14 +640,20 @@ __global__ void k_max_support(Graph g) {
 //   * the current buffer is zeroed over the vacated tail (a round that removes
 //     anything is not the converged one, so those counts are never returned).
 // Without it (host loop / observer) S is left untouched, as in the reference.
+// MODE 0 (prune): keep live slots with S >= k-2; the optional payload (slot
+// ids of the working layout) moves with col.
+// MODE 1 (publish): keep slots whose col is nonzero, moving S0 along -- the
+// caller-layout compaction after a degree-ordered fixpoint (see ktg_engine.cu).
+template <int MODE>
 __global__ void __launch_bounds__(kPruneThreads)
 k_prune_light(Graph g, int fused_reset) {
   const int lane = threadIdx.x & 31;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-  uint32_t* __restrict__ S = cur_S(g);
+  uint32_t* __restrict__ S = MODE ? g.S0 : cur_S(g);
   uint32_t* __restrict__ So = other_S(g);
   uint32_t* __restrict__ col = g.col;
+  uint32_t* __restrict__ pay = g.payload;
   const uint32_t thr = g.st->threshold;
   unsigned long long removed = 0;
   for (uint32_t v = warp + 1; v <= g.n; v += nwarps) {
@@ -571,27 +673,34 @@ k_prune_light(Graph g, int fused_reset) {
       const bool live = idx < d;
       const uint32_t c = live ? col[base + idx] : 0u;
       const uint32_t sv = live ? S[base + idx] : 0u;
-      const bool keep = live && sv >= thr;
+      const uint32_t pv = (live && pay) ? pay[base + idx] : 0u;
+      const bool keep = MODE ? (live && c != 0) : (live && sv >= thr);
       const unsigned m = __ballot_sync(0xffffffffu, keep);
       __syncwarp();  // every lane's loads precede any lane's in-place store
-      if (keep) col[base + write + __popc(m & ((1u << lane) - 1u))] = c;
-      if (fused_reset && live) So[base + idx] = 0;
+      const uint32_t at = base + write + __popc(m & ((1u << lane) - 1u));
+      if (keep) {
+        col[at] = c;
+        if (MODE) S[at] = sv;
+        if (pay) pay[at] = pv;
+      }
+      if (!MODE && fused_reset && live) So[base + idx] = 0;
       write += __popc(m);
     }
     for (uint32_t x = write + lane; x < d; x += 32) {
       col[base + x] = 0;
-      if (fused_reset) S[base + x] = 0;
+      if (MODE || fused_reset) S[base + x] = 0;
     }
     if (lane == 0) {
       g.deg[v] = write;
       removed += d - write;
     }
   }
-  if (lane == 0 && removed) atomicAdd(&g.st->removed, removed);
+  if (!MODE && lane == 0 && removed) atomicAdd(&g.st->removed, removed);
 }
 
 // CTA per heavy row (queued by k_prune_light): same compaction with a
 // block-wide scan over tiles of 4 * kPruneThreads slots.
+template <int MODE>
 __global__ void __launch_bounds__(kPruneThreads)
 k_prune_heavy(Graph g, int fused_reset) {
   __shared__ uint32_t red[kPruneThreads / 32];
@@ -601,9 +710,10 @@ k_prune_heavy(Graph g, int fused_reset) {
   const uint32_t tid = threadIdx.x;
   const int lane = tid & 31, wid = tid >> 5;
   constexpr int NW = kPruneThreads / 32;
-  uint32_t* __restrict__ S = cur_S(g);
+  uint32_t* __restrict__ S = MODE ? g.S0 : cur_S(g);
   uint32_t* __restrict__ So = other_S(g);
   uint32_t* __restrict__ col = g.col;
+  uint32_t* __restrict__ pay = g.payload;
   const uint32_t thr = g.st->threshold;
   const uint32_t nheavy = g.st->nheavy;
   unsigned long long removed = 0;
@@ -613,7 +723,7 @@ k_prune_heavy(Graph g, int fused_reset) {
     const uint32_t base = g.row_ptr[v];
     uint32_t write = 0;
     for (uint32_t off = 0; off < d; off += TILE) {
-      uint32_t c[EPT];
+      uint32_t c[EPT], sv[EPT], pv[EPT];
       bool keep[EPT];
       uint32_t cnt = 0;
 #pragma unroll
@@ -621,10 +731,11 @@ k_prune_heavy(Graph g, int fused_reset) {
         const uint32_t idx = off + tid * EPT + e;
         const bool live = idx < d;
         c[e] = live ? col[base + idx] : 0u;
-        const uint32_t sv = live ? S[base + idx] : 0u;
-        keep[e] = live && sv >= thr;
+        sv[e] = live ? S[base + idx] : 0u;
+        pv[e] = (live && pay) ? pay[base + idx] : 0u;
+        keep[e] = MODE ? (live && c[e] != 0) : (live && sv[e] >= thr);
         cnt += keep[e];
-        if (fused_reset && live) So[base + idx] = 0;
+        if (!MODE && fused_reset && live) So[base + idx] = 0;
       }
       uint32_t x = cnt;
 #pragma unroll
@@ -648,13 +759,18 @@ k_prune_heavy(Graph g, int fused_reset) {
       uint32_t pos = write + x - cnt + (wid ? red[wid - 1] : 0);
 #pragma unroll
       for (int e = 0; e < EPT; ++e)
-        if (keep[e]) col[base + pos++] = c[e];
+        if (keep[e]) {
+          col[base + pos] = c[e];
+          if (MODE) S[base + pos] = sv[e];
+          if (pay) pay[base + pos] = pv[e];
+          ++pos;
+        }
       write += tot_s;
       __syncthreads();
     }
     for (uint32_t x = write + tid; x < d; x += blockDim.x) {
       col[base + x] = 0;
-      if (fused_reset) S[base + x] = 0;
+      if (MODE || fused_reset) S[base + x] = 0;
     }
     if (tid == 0) {
       g.deg[v] = write;
@@ -662,7 +778,86 @@ k_prune_heavy(Graph g, int fused_reset) {
     }
     __syncthreads();
   }
-  if (tid == 0 && removed) atomicAdd(&g.st->removed, removed);
+  if (!MODE && tid == 0 && removed) atomicAdd(&g.st->removed, removed);
+}
+
+// ---------------------------------------------------------------------------
+// Degree-ordered working layout
+// ---------------------------------------------------------------------------
+// Vertices are ranked by (undirected degree, id); every edge is oriented from
+// lower to higher rank. Supports and trusses are orientation invariant, so the
+// fixpoint runs on this layout and the caller's layout is rebuilt from it at
+// the end (k_scatter_live + k_prune_*<1>) byte-identically.
+
+__global__ void k_rank_keys(const uint32_t* __restrict__ deg, const uint32_t* __restrict__ din, uint32_t n,
+                            unsigned long long* __restrict__ keys) {
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x + 1; v <= n; v += gridDim.x * blockDim.x)
+    keys[v - 1] = ((unsigned long long)(deg[v] + din[v]) << 32) | v;
+}
+
+__global__ void k_rank_assign(const unsigned long long* __restrict__ sorted, uint32_t n, uint32_t* __restrict__ rank) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    rank[(uint32_t)sorted[i]] = i + 1;
+}
+
+// Edge keys (a << B | b, a < b ranks) with the caller slot as value; warp per
+// caller row; offs = exclusive prefix of the caller live degrees.
+__global__ void k_edge_keys(Graph g, const uint32_t* __restrict__ rank, const uint32_t* __restrict__ offs,
+                            uint32_t B, unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals,
+                            uint32_t* __restrict__ cnt) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t u = warp + 1; u <= g.n; u += nwarps) {
+    const uint32_t d = g.deg[u], base = g.row_ptr[u], o = offs[u];
+    const uint32_t ru = rank[u];
+    for (uint32_t x = lane; x < d; x += 32) {
+      const uint32_t rv = rank[g.col[base + x]];
+      const uint32_t a = min(ru, rv), b = max(ru, rv);
+      keys[o + x] = ((unsigned long long)a << B) | b;
+      vals[o + x] = base + x;
+      atomicAdd(&cnt[a], 1u);
+    }
+  }
+}
+
+// row sizes (out-degree + sentinel) for the working row_ptr scan
+__global__ void k_row_sizes(const uint32_t* __restrict__ cnt, uint32_t n, uint32_t* __restrict__ sizes) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n + 2; i += gridDim.x * blockDim.x)
+    sizes[i] = (i >= 1 && i <= n) ? cnt[i] + 1 : 0;
+}
+
+// sorted (key, caller slot) -> working col / id; slot = idx + a - 1 because
+// every earlier row adds one sentinel.
+__global__ void k_fill_working(const unsigned long long* __restrict__ keys, const uint32_t* __restrict__ vals,
+                               uint64_t m, uint32_t B, uint32_t* __restrict__ col_w, uint32_t* __restrict__ id_w) {
+  const unsigned long long mask = (1ull << B) - 1;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = keys[i];
+    const uint32_t a = (uint32_t)(k >> B);
+    const uint64_t slot = i + a - 1;
+    col_w[slot] = (uint32_t)(k & mask);
+    id_w[slot] = vals[i];
+  }
+}
+
+// Publish, step 1: every live working slot writes its caller slot's pristine
+// column and its support into the (zeroed) caller arrays.
+__global__ void k_scatter_live(Graph w, const uint32_t* __restrict__ col_pristine, uint32_t* __restrict__ col_out,
+                               uint32_t* __restrict__ S_out, int add) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t* __restrict__ Sw = cur_S(w);
+  for (uint32_t a = warp + 1; a <= w.n; a += nwarps) {
+    const uint32_t d = w.deg[a], base = w.row_ptr[a];
+    for (uint32_t x = lane; x < d; x += 32) {
+      const uint32_t id = w.payload[base + x];
+      if (col_out) col_out[id] = col_pristine[id];
+      if (add) S_out[id] += Sw[base + x];
+      else S_out[id] = Sw[base + x];
+    }
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -729,12 +924,11 @@ __global__ void k_work_L(Graph g, const uint32_t* __restrict__ din, unsigned lon
 // ---------------------------------------------------------------------------
 // Extraction (extract_edges, csr.cpp:93-106): survivors as (u, v, S)
 // ---------------------------------------------------------------------------
-__global__ void k_extract(Graph g, const unsigned long long* __restrict__ offs, uint32_t* __restrict__ u,
-                          uint32_t* __restrict__ v, uint32_t* __restrict__ sup) {
+__global__ void k_extract(Graph g, const uint32_t* __restrict__ S, const unsigned long long* __restrict__ offs,
+                          uint32_t* __restrict__ u, uint32_t* __restrict__ v, uint32_t* __restrict__ sup) {
   const int lane = threadIdx.x & 31;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-  const uint32_t* __restrict__ S = cur_S(g);
   for (uint32_t r = warp + 1; r <= g.n; r += nwarps) {
     const uint32_t d = g.deg[r], base = g.row_ptr[r];
     const unsigned long long o = offs[r];

@@ -87,6 +87,7 @@ class TrussOptions:
     observer: Optional[RoundObserver] = None
     host_loop: bool = False
     naive_support: bool = False
+    label_order: bool = False   # run on the caller's CSR, not the degree-ordered copy
     device: int = -1
 
 
@@ -137,6 +138,7 @@ FLAG_HOST_LOOP = 1
 FLAG_NAIVE_SUPPORT = 2
 FLAG_COLLECT_WORK = 4
 FLAG_TIME_SUPPORT = 8
+FLAG_LABEL_ORDER = 16
 
 _configured = False
 
@@ -218,6 +220,8 @@ def _options(o: Optional[TrussOptions], keep=None) -> _Options:
         flags |= FLAG_HOST_LOOP
     if o.naive_support:
         flags |= FLAG_NAIVE_SUPPORT
+    if o.label_order:
+        flags |= FLAG_LABEL_ORDER
     c.flags = flags
     if o.observer is not None and keep is not None:
         obs = o.observer

@@ -27,9 +27,10 @@ def s14():
     return kt.rmat(14)
 
 
-def test_s14_every_k_byte_exact(s14, port):
+@pytest.mark.parametrize("label", [False, True])
+def test_s14_every_k_byte_exact(s14, port, label):
     ent = golden("rmat.json")["s14_known"]
-    eng = kt.Engine(s14)
+    eng = kt.Engine(s14, kt.TrussOptions(label_order=label))
     for k in range(3, ent["kmax"] + 2):
         eng.reset()
         hist = eng.run(k)
@@ -48,7 +49,8 @@ def test_s14_every_k_byte_exact(s14, port):
 
 def test_s14_naive_and_host_loop_agree(s14):
     base = kt.ktruss(s14, 5)
-    for o in (kt.TrussOptions(naive_support=True), kt.TrussOptions(host_loop=True)):
+    for o in (kt.TrussOptions(naive_support=True), kt.TrussOptions(host_loop=True),
+              kt.TrussOptions(label_order=True), kt.TrussOptions(label_order=True, naive_support=True)):
         r = kt.ktruss(s14, 5, o)
         assert np.array_equal(r.edges, base.edges) and r.removed_per_iteration == base.removed_per_iteration
 
@@ -127,9 +129,9 @@ def test_s20_known_answers_and_properties(s20):
     assert eng.info()["live_edges"] == ent["kmax_survivors"]
 
 
-@pytest.mark.parametrize("k", [3, 304])
-def test_s20_byte_exact(s20, port, k):
-    eng = kt.Engine(s20)
+@pytest.mark.parametrize("k,label", [(3, False), (304, False), (3, True)])
+def test_s20_byte_exact(s20, port, k, label):
+    eng = kt.Engine(s20, kt.TrussOptions(label_order=label))
     eng.reset()
     hist = eng.run(k)
     col, S = eng.read()

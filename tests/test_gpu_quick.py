@@ -15,11 +15,13 @@ def _graphs():
 
 
 @pytest.mark.parametrize("naive", [False, True])
-def test_supports_match_oracle(port, naive):
+@pytest.mark.parametrize("label", [False, True])
+def test_supports_match_oracle(port, naive, label):
     for name, g in _graphs():
         t_exp, S_exp = port.compute_supports(g, threads=4)
-        if naive:
-            eng = kt.Engine(g, kt.TrussOptions(naive_support=True))
+        if naive or label:
+            eng = kt.Engine(g, kt.TrussOptions(naive_support=naive, label_order=label))
+            eng.reset()
             t = eng.support_pass()
             _, S = eng.read()
         else:
@@ -31,13 +33,14 @@ def test_supports_match_oracle(port, naive):
 
 
 @pytest.mark.parametrize("host_loop", [False, True])
-def test_fixpoint_matches_oracle(port, host_loop):
+@pytest.mark.parametrize("label", [False, True])
+def test_fixpoint_matches_oracle(port, host_loop, label):
     for name, g in _graphs():
         for k in (2, 3, 4, 5, 8):
             col_e, S_e, hist_e = port.run_fixpoint(g, k, threads=4)
             work = g.copy()
             S = kt.SupportArray.zeros(g.total_slots())
-            hist = kt.run_fixpoint(work, S, k, kt.TrussOptions(host_loop=host_loop))
+            hist = kt.run_fixpoint(work, S, k, kt.TrussOptions(host_loop=host_loop, label_order=label))
             assert hist == hist_e, (name, k)
             assert np.array_equal(work.col_idx, col_e), (name, k)
             assert np.array_equal(S.counts, S_e), (name, k)
