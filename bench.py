@@ -262,7 +262,8 @@ def main():
     for k in mine:
         eng.reset()
         h = eng.run(k)
-        launches_per_k[k] = 2 + 6 * len(h)  # k_set_live + k_begin + 6 per round
+        # k_set_live + k_begin + 6 per round + 5 publish (degree-ordered layout)
+        launches_per_k[k] = 2 + 6 * len(h) + 5
 
     for _ in range(args.warmup):
         sweep(mine)

@@ -23,7 +23,7 @@ constexpr int kSupportThreads = 256; // threads per support CTA
 constexpr int kPruneThreads = 256;
 constexpr int kHeavyRow = 2048;      // rows longer than this are pruned by a CTA
 constexpr uint32_t kClipMin = 16;    // clip N+(j) by binary search above this degree
-constexpr uint32_t kScanRatio = 8;   // scan N+(j) if |N+(j)| <= ratio * |tail|
+constexpr uint32_t kScanRatio = 4;   // scan N+(j) if |N+(j)| <= ratio * |tail|
 constexpr int kHistCap = 1 << 16;    // recorded rounds per fixpoint
 
 // Device-resident loop state (one per engine).
@@ -230,6 +230,31 @@ __device__ __forceinline__ uint32_t filt_hash(uint32_t k, uint32_t te) {
   return ((k ^ (te * 0x85EBCA6Bu)) * 2654435761u) >> (32 - 15);
 }
 
+// Branchless lower_bound over a sorted run a[0, n) (n >= 1 not required):
+// first index with a[i] >= key, n if none.
+__device__ __forceinline__ uint32_t lb_smem(const uint32_t* a, uint32_t n, uint32_t key) {
+  if (n == 0) return 0;
+  const uint32_t* base = a;
+  while (n > 1) {
+    const uint32_t half = n >> 1;
+    base = (base[half] < key) ? base + half : base;
+    n -= half;
+  }
+  return (uint32_t)(base - a) + (*base < key);
+}
+
+__device__ __forceinline__ uint32_t lb_global(const uint32_t* __restrict__ a, uint32_t lo, uint32_t hi, uint32_t key) {
+  uint32_t n = hi - lo;
+  if (n == 0) return lo;
+  const uint32_t* base = a + lo;
+  while (n > 1) {
+    const uint32_t half = n >> 1;
+    base = (__ldg(base + half) < key) ? base + half : base;
+    n -= half;
+  }
+  return (uint32_t)(base - a) + (__ldg(base) < key);
+}
+
 // lower_bound in smem A[lo, hi)
 __device__ __forceinline__ uint32_t lower_bound_s(const uint32_t* A, uint32_t lo, uint32_t hi, uint32_t key) {
   uint32_t len = hi - lo;
@@ -281,7 +306,7 @@ __device__ __forceinline__ bool confirm(SupportSmem& s, uint32_t* __restrict__ S
                                         uint32_t k, uint32_t pos, uint32_t p) {
   const uint32_t te = s.te[p] & 0x7fffu;
   const uint32_t tb = diag ? p + 1 : 0;
-  const uint32_t x = lower_bound_s(s.A, tb, te, k);
+  const uint32_t x = tb + lb_smem(s.A + tb, te - tb, k);
   if (x < te && s.A[x] == k) {
     atomicAdd(&s.cntA[x], 1u);
     atomicAdd(&S[pos], 1u);
@@ -410,8 +435,8 @@ k_support_chunked(Graph g) {
               const uint32_t bs = g.row_ptr[j];
               uint32_t b0_ = bs, b1_ = bs + dj;
               if (dj > kClipMin) {
-                b0_ = lower_bound_g(col, bs, b1_, s.A[tb_]);
-                b1_ = upper_bound_g(col, b0_, b1_, s.A[te_ - 1]);
+                b0_ = lb_global(col, bs, b1_, s.A[tb_]);
+                b1_ = lb_global(col, b0_, b1_, s.A[te_ - 1] + 1);
               }
               const uint32_t blen = b1_ - b0_;
               if (blen) {
@@ -497,7 +522,7 @@ k_support_chunked(Graph g) {
           } else {
             const uint32_t x = (diag ? p + 1 : 0) + o;
             const uint32_t kk = s.A[x];
-            const uint32_t y = lower_bound_g(col, db0, db1, kk);
+            const uint32_t y = lb_global(col, db0, db1, kk);
             if (y < db1 && __ldg(col + y) == kk) {
               atomicAdd(&s.cntA[x], 1u);
               atomicAdd(&S[y], 1u);
