@@ -218,6 +218,16 @@ typedef int (*ktg_allreduce_cb)(uint32_t* d_buf, uint64_t count, void* stream, v
 ktg_status ktg_engine_set_partition(ktg_engine* e, uint32_t rank, uint32_t world,
                                     ktg_allreduce_cb allreduce, void* user);
 
+/* Native NCCL variant: the engine all-reduces its partial supports (u32 sum)
+ * and the round's triangle count (u64 sum) itself with ncclAllReduce on the
+ * engine stream, over NVLink/NVSwitch. Rank 0 creates the id with
+ * ktg_nccl_unique_id and ships the 128 bytes to every rank (e.g. through
+ * torch.distributed); every rank then calls ktg_engine_set_nccl
+ * (collective: blocks until all ranks joined). libnccl.so.2 is loaded with
+ * dlopen on first use. */
+ktg_status ktg_nccl_unique_id(uint8_t* out_128_bytes);
+ktg_status ktg_engine_set_nccl(ktg_engine* e, uint32_t rank, uint32_t world, const uint8_t* unique_id);
+
 #ifdef __cplusplus
 }
 #endif

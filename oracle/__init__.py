@@ -56,6 +56,8 @@ class _Port:
         L.orc_brute_supports.argtypes = [_u32, _vp, _u64, _vp]
         L.orc_random_graph_raw.argtypes = [_u32, ctypes.c_double, _u64, _vp]
         L.orc_random_graph_raw.restype = _u64
+        L.orc_support_tasks.argtypes = [_vp, _u32, _vp, _u64, _u32, _u32, _u32, _vp]
+        L.orc_support_tasks.restype = _u64
         self.L = L
 
     def compute_supports(self, g, supports=None, threads=1):
@@ -63,6 +65,14 @@ class _Port:
         col = _u32a(g.col_idx)
         t = self.L.orc_compute_supports(_p(_u32a(g.row_ptr)), g.num_vertices, _p(col), col.shape[0], _p(S),
                                         threads)
+        return int(t), S
+
+    def support_tasks(self, g, rank, world, chunk=1024):
+        """One rank's partial supports under the engine's task partition
+        (mirror of the device planner; see ktruss_oracle.c)."""
+        S = np.zeros(g.total_slots(), np.uint32)
+        t = self.L.orc_support_tasks(_p(_u32a(g.row_ptr)), g.num_vertices, _p(_u32a(g.col_idx)),
+                                     g.total_slots(), chunk, rank, world, _p(S))
         return int(t), S
 
     def intersect_tails(self, g, pivot, pred, S):

@@ -285,3 +285,75 @@ uint64_t orc_random_graph_raw(uint32_t n, double p, uint64_t seed, uint64_t* out
   }
   return 0;
 }
+
+/* ---- multi-GPU task partition (mirror of the device planner) -------------- */
+
+/* The engine's support tasks (paper_2009_07929_b200/csrc/ktg_kernels.cuh,
+ * k_plan_count / k_plan_write / k_support_chunked): the slot space is cut
+ * into `chunk`-slot chunks; off-diagonal tasks (q, q') for the last row of
+ * chunk q whose live part reaches chunk q' > q come first (q ascending, then
+ * q'), then the diagonal tasks (q, q). Task t belongs to rank t % world. A
+ * task processes the pivots of chunk q against the part of their a12 tails
+ * lying in chunk q'. This restatement computes one rank's partial supports
+ * with the reference's merge (support.cpp:64-91) restricted to that tail
+ * part. Returns the partial triangle count. S must be zero on entry. */
+static uint32_t row_of_slot(const uint32_t* row_ptr, uint32_t n, uint64_t s) {
+  uint32_t lo = 0, hi = n + 2;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (row_ptr[mid] <= s) lo = mid + 1; else hi = mid;
+  }
+  return lo - 1;
+}
+
+static uint64_t merge_range(const uint32_t* row_ptr, const uint32_t* col, uint64_t pivot, uint64_t t_lo,
+                            uint64_t t_hi, uint32_t* S) {
+  /* tail slots [t_lo, t_hi) of the pivot's row (stops at a zero) vs row col[pivot] */
+  uint64_t a = t_lo, b = row_ptr[col[pivot]];
+  uint32_t found = 0;
+  while (a < t_hi && col[a] != 0 && col[b] != 0) {
+    if (col[a] == col[b]) {
+      ++S[a];
+      ++S[b];
+      ++found;
+      ++a;
+      ++b;
+    } else if (col[b] > col[a]) {
+      ++a;
+    } else {
+      ++b;
+    }
+  }
+  S[pivot] += found;
+  return found;
+}
+
+uint64_t orc_support_tasks(const uint32_t* row_ptr, uint32_t n, const uint32_t* col, uint64_t slots,
+                           uint32_t chunk, uint32_t rank, uint32_t world, uint32_t* S) {
+  const uint64_t Q = (slots + chunk - 1) / chunk;
+  uint64_t t = 0, tri = 0;
+  /* off-diagonal tasks */
+  for (uint64_t q = 0; q < Q; ++q) {
+    const uint64_t e = ((q + 1) * chunk < slots ? (q + 1) * chunk : slots);
+    const uint32_t i = row_of_slot(row_ptr, n, e - 1);
+    if (i < 1) continue;
+    uint64_t le = row_ptr[i];
+    while (col[le] != 0) ++le; /* live end */
+    if (le <= e) continue;
+    const uint64_t last = (le - 1) / chunk;
+    for (uint64_t q2 = q + 1; q2 <= last; ++q2, ++t) {
+      if (t % world != rank) continue;
+      const uint64_t p_lo = row_ptr[i] > q * chunk ? row_ptr[i] : q * chunk;
+      const uint64_t a0 = q2 * chunk, a1 = (q2 + 1) * chunk < slots ? (q2 + 1) * chunk : slots;
+      for (uint64_t s = p_lo; s < e; ++s) tri += merge_range(row_ptr, col, s, a0, a1, S);
+    }
+  }
+  /* diagonal tasks */
+  for (uint64_t q = 0; q < Q; ++q, ++t) {
+    if (t % world != rank) continue;
+    const uint64_t p0 = q * chunk, p1 = (q + 1) * chunk < slots ? (q + 1) * chunk : slots;
+    for (uint64_t s = p0; s < p1; ++s)
+      if (col[s] != 0) tri += merge_range(row_ptr, col, s, s + 1, p1, S);
+  }
+  return tri;
+}

@@ -27,6 +27,8 @@
 #include <cuda_runtime.h>
 
 #include <cub/cub.cuh>
+#include <dlfcn.h>
+#include <nccl.h>
 
 #include <algorithm>
 #include <cstdio>
@@ -88,6 +90,36 @@ struct DBuf {
   }
 };
 
+// NCCL, loaded on first use (dlopen, so the library has no link-time NCCL
+// dependency; under PyTorch this resolves to the already-loaded libnccl.so.2).
+struct NcclApi {
+  bool ok = false;
+  decltype(&ncclGetUniqueId) getUniqueId = nullptr;
+  decltype(&ncclCommInitRank) commInitRank = nullptr;
+  decltype(&ncclAllReduce) allReduce = nullptr;
+  decltype(&ncclCommDestroy) commDestroy = nullptr;
+  decltype(&ncclGetErrorString) errorString = nullptr;
+};
+
+NcclApi* nccl_api() {
+  static NcclApi api;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (h) {
+      api.getUniqueId = (decltype(api.getUniqueId))dlsym(h, "ncclGetUniqueId");
+      api.commInitRank = (decltype(api.commInitRank))dlsym(h, "ncclCommInitRank");
+      api.allReduce = (decltype(api.allReduce))dlsym(h, "ncclAllReduce");
+      api.commDestroy = (decltype(api.commDestroy))dlsym(h, "ncclCommDestroy");
+      api.errorString = (decltype(api.errorString))dlsym(h, "ncclGetErrorString");
+      api.ok = api.getUniqueId && api.commInitRank && api.allReduce && api.commDestroy && api.errorString;
+    }
+  }
+  return api.ok ? &api : nullptr;
+}
+
 // One CSR orientation resident in HBM.
 struct Layout {
   uint32_t n = 0;
@@ -146,6 +178,7 @@ struct ktg_engine {
   uint32_t scan_ratio = kScanRatio;
   ktg_allreduce_cb allreduce = nullptr;
   void* allreduce_user = nullptr;
+  ncclComm_t nccl = nullptr;
 
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evs0 = nullptr, evs1 = nullptr;
   ktg_run_info info{};
@@ -437,11 +470,18 @@ ktg_status enqueue_round(ktg_engine* e, bool graph_mode, cudaGraphConditionalHan
   if (sup1) KTG_CUDA(cudaEventRecord(sup1, s));
   if (e->opt.width_bits == 16) k_check16<<<4 * e->num_sms, 256, 0, s>>>(g);
   KTG_CUDA(cudaGetLastError());
-  if (!graph_mode && e->world > 1 && e->allreduce) {
+  if (!graph_mode && (e->nccl || (e->world > 1 && e->allreduce))) {
     // partial supports of this rank's task share -> full supports everywhere
     uint32_t* buf = e->h_st->parity ? L.S1.p : L.S0.p;
-    if (e->allreduce(buf, L.slots, e->stream, e->allreduce_user) != 0)
+    if (e->nccl) {
+      NcclApi* api = nccl_api();
+      ncclResult_t r = api->allReduce(buf, buf, L.slots, ncclUint32, ncclSum, e->nccl, e->stream);
+      if (r == ncclSuccess)
+        r = api->allReduce(&e->d_st->triangles, &e->d_st->triangles, 1, ncclUint64, ncclSum, e->nccl, e->stream);
+      if (r != ncclSuccess) return fail(KTG_ERR_CUDA, std::string("ncclAllReduce: ") + api->errorString(r));
+    } else if (e->allreduce(buf, L.slots, e->stream, e->allreduce_user) != 0) {
       return fail(KTG_ERR_CUDA, "allreduce callback failed");
+    }
   }
   k_prune_light<0><<<e->prune_grid, kPruneThreads, 0, s>>>(g, fused);
   k_prune_heavy<0><<<e->heavy_grid, kPruneThreads, 0, s>>>(g, fused);
@@ -527,7 +567,8 @@ ktg_status run_loop(ktg_engine* e, bool want_sync) {
   Layout& L = e->act();
   const bool timing = flag(e, KTG_FLAG_TIME_SUPPORT);
   const bool recording = timing || flag(e, KTG_FLAG_COLLECT_WORK);
-  const bool host_loop = flag(e, KTG_FLAG_HOST_LOOP) || e->opt.observer || (e->world > 1) || recording;
+  const bool host_loop =
+      flag(e, KTG_FLAG_HOST_LOOP) || e->opt.observer || (e->world > 1) || e->nccl || recording;
   e->work.clear();
   e->caller_stale = true;
   KTG_CUDA(cudaEventRecord(e->ev0, e->stream));
@@ -783,6 +824,7 @@ ktg_status ktg_engine_create(const ktg_options* opt, ktg_engine** out) {
 void ktg_engine_destroy(ktg_engine* e) {
   if (!e) return;
   if (e->stream) cudaStreamSynchronize(e->stream);
+  if (e->nccl && nccl_api()) nccl_api()->commDestroy(e->nccl);
   e->free_all();
   if (e->d_st) cudaFree(e->d_st);
   if (e->d_hist) cudaFree(e->d_hist);
@@ -870,6 +912,38 @@ ktg_status ktg_engine_set_partition(ktg_engine* e, uint32_t rank, uint32_t world
   e->world = world;
   e->allreduce = allreduce;
   e->allreduce_user = user;
+  if (e->exec) cudaGraphExecDestroy(e->exec);
+  e->exec = nullptr;
+  return KTG_OK;
+}
+
+ktg_status ktg_nccl_unique_id(uint8_t* out) {
+  NcclApi* api = nccl_api();
+  if (!api) return fail(KTG_ERR_CUDA, "libnccl.so.2 not loadable");
+  ncclUniqueId id;
+  const ncclResult_t r = api->getUniqueId(&id);
+  if (r != ncclSuccess) return fail(KTG_ERR_CUDA, std::string("ncclGetUniqueId: ") + api->errorString(r));
+  std::memcpy(out, &id, sizeof(id));
+  return KTG_OK;
+}
+
+ktg_status ktg_engine_set_nccl(ktg_engine* e, uint32_t rank, uint32_t world, const uint8_t* unique_id) {
+  if (world == 0 || rank >= world) return fail(KTG_ERR_INVALID_PARAMETER, "rank must be < world");
+  NcclApi* api = nccl_api();
+  if (!api) return fail(KTG_ERR_CUDA, "libnccl.so.2 not loadable");
+  if (e->nccl) api->commDestroy(e->nccl);
+  e->nccl = nullptr;
+  ncclUniqueId id;
+  std::memcpy(&id, unique_id, sizeof(id));
+  KTG_CUDA(cudaSetDevice(e->device));
+  const ncclResult_t r = api->commInitRank(&e->nccl, (int)world, id, (int)rank);
+  if (r != ncclSuccess) {
+    e->nccl = nullptr;
+    return fail(KTG_ERR_CUDA, std::string("ncclCommInitRank: ") + api->errorString(r));
+  }
+  e->rank_id = rank;
+  e->world = world;
+  e->allreduce = nullptr;
   if (e->exec) cudaGraphExecDestroy(e->exec);
   e->exec = nullptr;
   return KTG_OK;

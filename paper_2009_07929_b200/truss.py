@@ -178,6 +178,8 @@ def lib():
         L.ktg_engine_device_state.argtypes = [_vp, P(_vp), P(_vp), P(_vp)]
         L.ktg_engine_extract.argtypes = [_vp, _vp, _vp, _vp, _u64, P(_u64)]
         L.ktg_engine_set_partition.argtypes = [_vp, _u32, _u32, ALLREDUCE_CB, _vp]
+        L.ktg_nccl_unique_id.argtypes = [_vp]
+        L.ktg_engine_set_nccl.argtypes = [_vp, _u32, _u32, _vp]
         _configured = True
     return L
 
@@ -379,6 +381,13 @@ class detail:  # namespace ktruss::detail (truss.hpp:58-63)
 # Device-resident engine (what the benchmark times)
 # ---------------------------------------------------------------------------
 
+def nccl_unique_id() -> bytes:
+    """ncclGetUniqueId (128 bytes) for Engine.set_nccl."""
+    buf = (ctypes.c_uint8 * 128)()
+    _check(lib().ktg_nccl_unique_id(buf))
+    return bytes(buf)
+
+
 class Engine:
     """A graph resident in HBM with its pristine copy; ktg_engine_* calls."""
 
@@ -490,6 +499,11 @@ class Engine:
         num = _u64()
         _check(lib().ktg_engine_extract(self._h, _p(out[0]), _p(out[1]), _p(out[2]), cap, ctypes.byref(num)))
         return np.ascontiguousarray(out[:, :int(num.value)].T)
+
+    def set_nccl(self, rank: int, world: int, unique_id: bytes) -> None:
+        """Edge-partitioned fixpoint over NCCL (collective across ranks)."""
+        buf = (ctypes.c_uint8 * 128).from_buffer_copy(unique_id)
+        _check(lib().ktg_engine_set_nccl(self._h, rank, world, buf))
 
     def set_partition(self, rank: int, world: int, allreduce=None) -> None:
         cb = ALLREDUCE_CB(allreduce) if allreduce is not None else ALLREDUCE_CB()

@@ -138,3 +138,31 @@ def test_s20_byte_exact(s20, port, k, label):
     col_e, S_e, hist_e = port.run_fixpoint(s20, k, threads=16)
     assert hist == hist_e
     assert np.array_equal(col, col_e) and np.array_equal(S, S_e)
+
+
+def test_rank_partials_match_oracle_task_partition(port):
+    """Each rank's partial supports (device task share t % world == rank)
+    equal the oracle's mirror of the device planner, rank by rank."""
+    g = kt.rmat(12, 16, seed=9)
+    for world in (2, 3):
+        for r in range(world):
+            e = kt.Engine(g, kt.TrussOptions(label_order=True))
+            e.set_partition(r, world, allreduce=lambda *a: 0)
+            e.reset()
+            t = e.support_pass()
+            t_o, S_o = port.support_tasks(g, r, world)
+            assert t == t_o and np.array_equal(e.read()[1], S_o), (world, r)
+
+
+def test_nccl_single_rank_fixpoint(port):
+    """The native ncclAllReduce path (world of 1 on this box) runs the
+    host-driven partitioned loop byte-exactly."""
+    g = kt.rmat(13, 16, seed=4)
+    e = kt.Engine(g)
+    e.set_nccl(0, 1, kt.truss.nccl_unique_id())
+    for k in (3, 7):
+        e.reset()
+        hist = e.run(k)
+        col, S = e.read()
+        col_e, S_e, hist_e = port.run_fixpoint(g, k, threads=8)
+        assert hist == hist_e and np.array_equal(col, col_e) and np.array_equal(S, S_e)
