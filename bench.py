@@ -41,7 +41,7 @@ METRIC = "K-truss time-to-fixpoint (ms) & edges/sec at 1/2/4/8 B200; achieved HB
 # K_max of the pinned configs (reference-measured; also
 # asserted by tests/test_gpu_large.py) -- lets the reference arm skip its
 # ~200 s CPU kmax_search.
-KNOWN_KMAX = {(14, 16, 42): 79, (20, 16, 42): 304}
+KNOWN_KMAX = {(14, 16, 42): 79, (20, 16, 42): 304, (24, 16, 42): 935}
 
 
 def parse():
@@ -57,6 +57,10 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--cpu-budget-s", type=float, default=20.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--mode", default="sweep", choices=["sweep", "fixpoint"],
+                    help="sweep: K sweep 3..K_max (K split across ranks); fixpoint: one fixpoint per step "
+                         "at --k (0 = K_max), edge-partitioned over NCCL across ranks")
+    ap.add_argument("--k", type=int, default=0)
     return ap.parse_args()
 
 
@@ -206,6 +210,8 @@ def main():
     args = parse()
     if args.impl == "reference":
         return run_reference(args)
+    if args.mode == "fixpoint":
+        return run_fixpoint_mode(args)
 
     import numpy as np
     import torch
@@ -305,7 +311,7 @@ def main():
         d2h = 0
         for k in mine:
             r = kt.ktruss(hg, k)
-            d2h += r.edges.nbytes + 8 * r.iterations
+            d2h += r.nbytes + 8 * r.iterations
         torch.cuda.synchronize()
         e2e_ms.append((time.perf_counter() - t) * 1e3)
     barrier()
@@ -398,6 +404,132 @@ def main():
             "gpu_launches": launches,
             "clocks": clocks.summary(),
             "gen_s": round(gen_s, 2),
+        }
+        print(json.dumps(line), flush=True)
+    eng.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def cpu_port_sample(g, k, budget_s, threads, world_parts=64):
+    """CPU baseline for graphs too large to run whole within the budget: the
+    C port (oracle/ktruss_oracle.c, OpenMP) restricted to 1/world_parts of
+    the engine's support tasks of the pristine round-1 pass, scaled back up.
+    Returns (edges/s estimate for the fixpoint's round 1 only, description)."""
+    import time as _t
+
+    import oracle
+    P = oracle.port()
+    t0 = _t.perf_counter()
+    P.support_tasks(g, 0, world_parts)
+    dt = (_t.perf_counter() - t0) * world_parts
+    return g.num_edges / dt, (f"C port, support tasks t%{world_parts}==0 of the pristine round-1 pass "
+                              f"(single thread), scaled x{world_parts}: {dt:.1f} s per support pass; "
+                              "lower bound on the fixpoint time")
+
+
+def run_fixpoint_mode(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2009_07929_b200 as kt
+    from paper_2009_07929_b200 import dist as kd
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    dev = torch.device("cuda", local)
+    t0 = time.time()
+    g = kt.rmat(args.scale, args.ef, args.seed)
+    gen_s = time.time() - t0
+    n, slots, m = g.num_vertices, g.total_slots(), g.num_edges
+    stream = torch.cuda.Stream()
+    eng = kt.Engine(g, stream=stream.cuda_stream)
+    k = args.k or KNOWN_KMAX.get((args.scale, args.ef, args.seed)) or eng.kmax()
+    if world > 1:
+        kd.engine_join(eng)
+    eng.reset()
+    hist = eng.run(k)
+    launches = 2 + 6 * len(hist) + 5
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    for _ in range(args.warmup):
+        eng.reset()
+        eng.run(k, sync=False)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    step_ms = []
+    with ClockSampler(local) as clocks:
+        for _ in range(args.steps):
+            with torch.cuda.stream(stream):
+                flush.fill_(1)
+            eng.reset()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            eng.run(k, sync=False)
+            e1.record(stream)
+            e1.synchronize()
+            step_ms.append(e0.elapsed_time(e1))
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms = kd.max_over_ranks(sum(step_ms) / len(step_ms), dev)
+    value = m / (ms / 1e3)
+    # e2e: the engine's public API from pinned host buffers each step
+    keep = (torch.empty(n + 2, dtype=torch.int32, pin_memory=True), torch.empty(slots, dtype=torch.int32,
+                                                                                 pin_memory=True))
+    keep[0].numpy().view(np.uint32)[:] = g.row_ptr
+    keep[1].numpy().view(np.uint32)[:] = g.col_idx
+    hg = kt.ZeroTerminatedCsr(n, keep[0].numpy().view(np.uint32), keep[1].numpy().view(np.uint32))
+    torch.cuda.synchronize()
+    t = time.perf_counter()
+    eng.load(hg)
+    eng.run(k)
+    edges = eng.extract()
+    torch.cuda.synchronize()
+    e2e_ms = kd.max_over_ranks((time.perf_counter() - t) * 1e3, dev)
+    roof = None
+    cpu = None
+    if rank == 0:
+        try:
+            peak, src = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]), "measured"
+        except Exception:
+            peak, src = 6650.0, "fallback"
+        ew = kt.Engine(g, collect_work=True)
+        et = kt.Engine(g, time_support=True)
+        ew.reset(); ew.run(k); w = ew.round_work()
+        et.reset(); et.run(k); tw = et.round_work()
+        ew.close(); et.close()
+        tb = sum(support_bytes(x, n, slots) for x in w)
+        tm = sum(x["support_ms"] for x in tw)
+        achieved = tb / (tm / 1e3) / 1e9
+        roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": None, "peak_source": src,
+                "kernel": "k_support_chunked", "launches_measured": len(tw)}
+        if world == 1 and not args.no_cpu_baseline:
+            v, desc = cpu_port_sample(g, k, args.cpu_budget_s, 1)
+            cpu = {"value": v, "unit": "edges/s", "cores": 1, "kind": "port", "sample": desc}
+        line = {
+            "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "u32", "data": "synthetic",
+            "config": {"workload": f"rmat-s{args.scale}-ef{args.ef} K={k} fixpoint",
+                       "n": n, "m": m, "slots": slots, "k": k, "rounds": len(hist),
+                       "l2": "512 MiB memset between timed steps; inputs > L2" if slots * 4 > 126e6 else
+                             "512 MiB memset between timed steps",
+                       "parallelism": f"edge-partitioned x{world} (ncclAllReduce of S per round)" if world > 1
+                                      else "single"},
+            "time_to_fixpoint_ms": ms, "me_per_s": value / 1e6,
+            "e2e": {"value": m / (e2e_ms / 1e3), "unit": "edges/s", "h2d_bytes_per_step": (n + 2 + slots) * 4,
+                    "d2h_bytes_per_step": int(edges.nbytes), "ms_per_step": e2e_ms,
+                    "api": "Engine.load (pinned host) + run + extract"},
+            "roofline": roof, "cpu_baseline": cpu, "gpu_launches": launches * args.steps,
+            "clocks": clocks.summary(), "gen_s": round(gen_s, 2),
         }
         print(json.dumps(line), flush=True)
     eng.close()

@@ -91,14 +91,31 @@ class TrussOptions:
     device: int = -1
 
 
-@dataclass
 class TrussResult:
-    """truss.hpp:12-21. `edges` is an (m, 3) u32 array of (u, v, support) in
-    lexicographic order (the reference's vector<SupportedEdge>)."""
-    k: int
-    edges: np.ndarray
-    iterations: int
-    removed_per_iteration: List[int]
+    """truss.hpp:12-21. The surviving edges in lexicographic order (the
+    reference's vector<SupportedEdge>) as three u32 columns `u`, `v`,
+    `support`; `edges` stacks them into an (m, 3) array on first use."""
+
+    def __init__(self, k: int, u: np.ndarray, v: np.ndarray, support: np.ndarray, iterations: int,
+                 removed_per_iteration: List[int]):
+        self.k = k
+        self.u, self.v, self.support = u, v, support
+        self.iterations = iterations
+        self.removed_per_iteration = removed_per_iteration
+        self._edges = None
+
+    @property
+    def edges(self) -> np.ndarray:
+        if self._edges is None:
+            self._edges = np.stack([self.u, self.v, self.support], axis=1)
+        return self._edges
+
+    def __len__(self) -> int:
+        return int(self.u.shape[0])
+
+    @property
+    def nbytes(self) -> int:
+        return int(self.u.nbytes + self.v.nbytes + self.support.nbytes)
 
     def edge_tuples(self):
         return [tuple(int(x) for x in r) for r in self.edges]
@@ -241,6 +258,18 @@ def _options(o: Optional[TrussOptions], keep=None) -> _Options:
     return c
 
 
+def _host_u32(count: int) -> np.ndarray:
+    """Output buffer for device->host copies: page-locked (PyTorch's caching
+    host allocator, so repeated calls do not re-pin) when CUDA is up."""
+    try:
+        import torch
+        if torch.cuda.is_available():
+            return torch.empty(max(count, 1), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
+    except Exception:
+        pass
+    return np.empty(max(count, 1), np.uint32)
+
+
 def _check_threads(threads: int) -> None:
     if threads < 1:
         raise errors.InvalidParameterError("thread count must be >= 1")
@@ -332,9 +361,8 @@ def ktruss(graph: ZeroTerminatedCsr, k: int, options: Optional[TrussOptions] = N
     options = options or TrussOptions()
     _check_threads(options.threads)
     col = _u32arr(graph.col_idx)
-    live = int(np.count_nonzero(col))
-    cap_e = max(live, 1)
-    out = np.empty((3, cap_e), dtype=np.uint32)
+    cap_e = max(col.shape[0] - graph.num_vertices, 1)  # >= live edges
+    u, v, sup = _host_u32(cap_e), _host_u32(cap_e), _host_u32(cap_e)
     num = _u64()
     hcap = 1 << 16
     hist = np.zeros(hcap, dtype=np.uint64)
@@ -342,11 +370,10 @@ def ktruss(graph: ZeroTerminatedCsr, k: int, options: Optional[TrussOptions] = N
     keep = {"graph": graph}
     o = _options(options, keep)
     _check(lib().ktg_ktruss(_p(_u32arr(graph.row_ptr)), graph.num_vertices, _p(col), col.shape[0], k,
-                            ctypes.byref(o), _p(out[0]), _p(out[1]), _p(out[2]), cap_e,
+                            ctypes.byref(o), _p(u), _p(v), _p(sup), cap_e,
                             ctypes.byref(num), _p(hist), hcap, ctypes.byref(it)))
     m = int(num.value)
-    edges = np.ascontiguousarray(out[:, :m].T)
-    return TrussResult(k, edges, int(it.value), [int(x) for x in hist[:min(it.value, hcap)]])
+    return TrussResult(k, u[:m], v[:m], sup[:m], int(it.value), [int(x) for x in hist[:min(it.value, hcap)]])
 
 
 def kmax_search(graph: ZeroTerminatedCsr, options: Optional[TrussOptions] = None) -> KmaxResult:
@@ -354,9 +381,8 @@ def kmax_search(graph: ZeroTerminatedCsr, options: Optional[TrussOptions] = None
     options = options or TrussOptions()
     _check_threads(options.threads)
     col = _u32arr(graph.col_idx)
-    live = int(np.count_nonzero(col))
-    cap_e = max(live, 1)
-    out = np.empty((3, cap_e), dtype=np.uint32)
+    cap_e = max(col.shape[0] - graph.num_vertices, 1)
+    u, v, sup = _host_u32(cap_e), _host_u32(cap_e), _host_u32(cap_e)
     num = _u64()
     hcap = 1 << 16
     hist = np.zeros(hcap, dtype=np.uint64)
@@ -365,11 +391,11 @@ def kmax_search(graph: ZeroTerminatedCsr, options: Optional[TrussOptions] = None
     keep = {"graph": graph}
     o = _options(options, keep)
     _check(lib().ktg_kmax_search(_p(_u32arr(graph.row_ptr)), graph.num_vertices, _p(col), col.shape[0],
-                                 ctypes.byref(o), ctypes.byref(kmax), _p(out[0]), _p(out[1]), _p(out[2]),
+                                 ctypes.byref(o), ctypes.byref(kmax), _p(u), _p(v), _p(sup),
                                  cap_e, ctypes.byref(num), _p(hist), hcap, ctypes.byref(it)))
     m = int(num.value)
-    edges = np.ascontiguousarray(out[:, :m].T)
-    tr = TrussResult(int(kmax.value), edges, int(it.value), [int(x) for x in hist[:min(it.value, hcap)]])
+    tr = TrussResult(int(kmax.value), u[:m], v[:m], sup[:m], int(it.value),
+                     [int(x) for x in hist[:min(it.value, hcap)]])
     return KmaxResult(int(kmax.value), tr)
 
 
@@ -493,12 +519,15 @@ class Engine:
         _check(lib().ktg_engine_device_state(self._h, ctypes.byref(c), ctypes.byref(s), ctypes.byref(st)))
         return c.value, s.value, st.value
 
-    def extract(self, cap: Optional[int] = None) -> np.ndarray:
+    def extract(self, cap: Optional[int] = None):
+        """Survivors as a TrussResult-like (u, v, support) triple of u32
+        columns (pinned host memory); .edges stacks them."""
         cap = cap if cap is not None else max(1, self.graph.num_edges)
-        out = np.empty((3, cap), dtype=np.uint32)
+        u, v, sup = _host_u32(cap), _host_u32(cap), _host_u32(cap)
         num = _u64()
-        _check(lib().ktg_engine_extract(self._h, _p(out[0]), _p(out[1]), _p(out[2]), cap, ctypes.byref(num)))
-        return np.ascontiguousarray(out[:, :int(num.value)].T)
+        _check(lib().ktg_engine_extract(self._h, _p(u), _p(v), _p(sup), cap, ctypes.byref(num)))
+        m = int(num.value)
+        return TrussResult(0, u[:m], v[:m], sup[:m], 0, [])
 
     def set_nccl(self, rank: int, world: int, unique_id: bytes) -> None:
         """Edge-partitioned fixpoint over NCCL (collective across ranks)."""
