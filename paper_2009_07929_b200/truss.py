@@ -489,6 +489,28 @@ class Engine:
         self.run(lo)
         return lo
 
+    def sweep(self, k_lo: int = 3, k_hi: Optional[int] = None, extract: bool = False):
+        """Incremental K sweep: K = k_lo, k_lo+1, ... each
+        fixpoint starting from the previous K's truss instead of the pristine
+        graph. The k-truss is unique and trusses are nested, so every K's
+        survivors and supports equal ktruss(graph, K) from pristine (tested);
+        only `iterations` differ. Stops after k_hi or at the first empty
+        truss (that K is K_max + 1 and is included). Returns a list of dicts
+        (k, live_edges, iterations[, truss])."""
+        self.reset()
+        out = []
+        k = k_lo
+        while k_hi is None or k <= k_hi:
+            hist = self.run(k)
+            rec = {"k": k, "live_edges": int(self.info()["live_edges"]), "iterations": len(hist)}
+            if extract:
+                rec["truss"] = self.extract()
+            out.append(rec)
+            if rec["live_edges"] == 0:
+                break
+            k += 1
+        return out
+
     def support_pass(self) -> int:
         tri = _u64()
         _check(lib().ktg_engine_support_pass(self._h, ctypes.byref(tri)))

@@ -166,3 +166,15 @@ def test_nccl_single_rank_fixpoint(port):
         col, S = e.read()
         col_e, S_e, hist_e = port.run_fixpoint(g, k, threads=8)
         assert hist == hist_e and np.array_equal(col, col_e) and np.array_equal(S, S_e)
+
+
+def test_incremental_sweep_equals_pristine(s14, port):
+    """Engine.sweep: every K's truss (edges + supports) equals the pristine
+    ktruss(K); the sweep ends at K_max + 1 (empty)."""
+    ent = golden("rmat.json")["s14_known"]
+    eng = kt.Engine(s14)
+    recs = eng.sweep(3, extract=True)
+    assert recs[-1]["live_edges"] == 0 and recs[-1]["k"] == ent["kmax"] + 1
+    for rec in recs[::7] + [recs[-2]]:
+        e, _ = port.truss_edges(s14, rec["k"], threads=8)
+        assert np.array_equal(rec["truss"].edges, e), rec["k"]
