@@ -45,6 +45,7 @@ typedef enum {
   KTG_ERR_INVALID_PARAMETER = 1, /* ktruss::InvalidParameterError            */
   KTG_ERR_SUPPORT_OVERFLOW = 2,  /* ktruss::SupportOverflowError; slot via ktg_last_error_slot() */
   KTG_ERR_INVALID_INPUT = 3,     /* ktruss::InvalidInputError                */
+  KTG_ERR_CORRUPT_CACHE = 4,     /* ktruss::CorruptCacheError                */
   KTG_ERR_CUDA = 5,              /* CUDA runtime / NCCL failure              */
   KTG_ERR_NO_DEVICE = 6,         /* no usable sm_100 device                  */
   KTG_ERR_OOM = 7                /* device or host allocation failed         */
@@ -183,6 +184,11 @@ ktg_status ktg_engine_load(ktg_engine* e, const uint32_t* row_ptr, uint32_t n,
 /* Same, from device pointers (D2D). */
 ktg_status ktg_engine_load_device(ktg_engine* e, const uint32_t* d_row_ptr, uint32_t n,
                                   const uint32_t* d_col_idx, uint64_t slots);
+/* ZTCSR1 cache file straight into HBM (read_csr_cache, csr_cache.hpp:19-21,
+ * csr_cache.cpp:80-111): streamed through pinned staging buffers, structural
+ * invariants validated on the device. Errors: KTG_ERR_CORRUPT_CACHE with the
+ * reference's messages. */
+ktg_status ktg_engine_load_cache(ktg_engine* e, const char* path);
 /* Restores the pristine col_idx and zeroes both support buffers (async on
  * the engine stream). */
 ktg_status ktg_engine_reset(ktg_engine* e);

@@ -26,6 +26,8 @@ enum {
   KTGG_ERR_INVALID_PARAMETER = 1,
   KTGG_ERR_INVALID_INPUT = 3,
   KTGG_ERR_EMPTY_GRAPH = 4,
+  KTGG_ERR_CORRUPT_CACHE = 5,
+  KTGG_ERR_IO = 6,
   KTGG_ERR_OOM = 7
 };
 
@@ -65,6 +67,18 @@ uint64_t ktgg_csr_slots(const ktgg_csr* c);
  * unused); any pointer may be NULL. */
 void ktgg_csr_copy(const ktgg_csr* c, uint32_t* row_ptr, uint32_t* col, uint64_t* original_ids);
 void ktgg_csr_free(ktgg_csr* c);
+
+/* ZTCSR1 binary cache <- write_csr_cache / read_csr_cache (csr_cache.hpp:16-21,
+ * csr_cache.cpp:71-111): "ZTCSR1\0\0" | u32 n | u64 slots | row_ptr | col_idx,
+ * little-endian. The reader validates like the reference (KTGG_ERR_CORRUPT_CACHE
+ * with the reference's messages). */
+int ktgg_write_csr_cache(const char* path, const uint32_t* row_ptr, uint32_t n, const uint32_t* col,
+                         uint64_t slots);
+int ktgg_read_csr_cache(const char* path, ktgg_csr** out);
+
+/* validate_csr (csr.hpp:32, csr.cpp:34-80): KTGG_OK or KTGG_ERR_INVALID_INPUT
+ * with the reference's message for the first violation. */
+int ktgg_validate_csr(const uint32_t* row_ptr, uint64_t rp_len, uint32_t n, const uint32_t* col, uint64_t slots);
 
 /* Closed-form merge work of one support pass over the live graph. */
 void ktgg_round_work(const uint32_t* row_ptr, uint32_t n, const uint32_t* col, ktgg_work* w);

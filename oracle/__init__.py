@@ -170,6 +170,8 @@ class _Ref:
         L.ref_oracle_truss.argtypes = [_vp, _u32, _vp, _u64, _u32, _vp, _vp, _vp]
         L.ref_oracle_truss.restype = _u64
         L.ref_hardware_threads.restype = ctypes.c_int
+        L.ref_write_csr_cache.argtypes = [ctypes.c_char_p, _vp, _u32, _vp, _u64]
+        L.ref_read_csr_cache.argtypes = [ctypes.c_char_p, _P(_vp)]
         self.L = L
 
     def _err(self, rc):
@@ -251,6 +253,18 @@ class _Ref:
         self._err(self.L.ref_kmax_search(_p(_u32a(g.row_ptr)), g.num_vertices, _p(_u32a(g.col_idx)),
                                          g.total_slots(), strategy, threads, ctypes.byref(h)))
         return self._truss(h)
+
+    def write_cache(self, g, path):
+        self._err(self.L.ref_write_csr_cache(path.encode(), _p(_u32a(g.row_ptr)), g.num_vertices,
+                                             _p(_u32a(g.col_idx)), g.total_slots()))
+
+    def read_cache(self, path):
+        """(graph, None) or (None, CorruptCacheError message)."""
+        h = _vp()
+        rc = self.L.ref_read_csr_cache(path.encode(), ctypes.byref(h))
+        if rc:
+            return None, self.L.ref_last_error().decode()
+        return self._csr(h), None
 
     def validate(self, g):
         rc = self.L.ref_validate_csr(_p(_u32a(g.row_ptr)), g.num_vertices, _p(_u32a(g.col_idx)), g.total_slots())

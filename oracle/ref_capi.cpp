@@ -20,7 +20,11 @@
 #include <string>
 #include <vector>
 
+#include <fstream>
+#include <sstream>
+
 #include "ktruss/bench.hpp"
+#include "ktruss/csr_cache.hpp"
 #include "ktruss/csr.hpp"
 #include "ktruss/edge_list.hpp"
 #include "ktruss/errors.hpp"
@@ -276,6 +280,38 @@ std::uint64_t ref_oracle_truss(const std::uint32_t* row_ptr, std::uint32_t n,
     s[i] = sup.at(survivors[i]);
   }
   return survivors.size();
+}
+
+// write_csr_cache / read_csr_cache (csr_cache.cpp:71-111) to / from a file.
+int ref_write_csr_cache(const char* path, const std::uint32_t* row_ptr, std::uint32_t n, const std::uint32_t* col,
+                        std::uint64_t slots) {
+  try {
+    std::ofstream out(path, std::ios::binary);
+    write_csr_cache(make_csr(row_ptr, n, col, slots), out);
+    return 0;
+  } catch (const std::exception& e) {
+    return code_of(e);
+  }
+}
+
+int ref_read_csr_cache(const char* path, void** out) {
+  try {
+    std::ifstream in(path, std::ios::binary);
+    auto* c = new CsrOut;
+    try {
+      c->csr = read_csr_cache(in);
+    } catch (...) {
+      delete c;
+      throw;
+    }
+    *out = c;
+    return 0;
+  } catch (const CorruptCacheError& e) {
+    g_err = e.what();
+    return 7;
+  } catch (const std::exception& e) {
+    return code_of(e);
+  }
 }
 
 double ref_millions_of_edges_per_second(std::uint64_t edges, double ms) {

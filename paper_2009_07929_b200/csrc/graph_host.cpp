@@ -18,6 +18,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <cstdio>
 #include <cstring>
 #include <limits>
 #include <new>
@@ -199,6 +200,38 @@ int canonical_csr(const T* raw, std::uint64_t m, Csr& out) {
 
 inline double unit53(std::mt19937_64& g) { return static_cast<double>(g() >> 11) * 0x1.0p-53; }
 
+// validate_csr (csr.cpp:34-80), same checks in the same order, same messages.
+// Returns an empty string when valid.
+std::string validate(std::uint32_t n, const std::uint32_t* rp, std::uint64_t rp_len, const std::uint32_t* col,
+                     std::uint64_t slots) {
+  if (n == 0) return "csr has no vertices";
+  if (rp_len != n + 2ull) return "row_ptr must have num_vertices + 2 entries";
+  if (rp[0] != 0 || rp[1] != 0) return "phantom vertex 0 must own no slots";
+  if (slots > 0xFFFFFFFFull) return "slot count exceeds 32-bit offsets";
+  if (rp[n + 1] != slots) return "row_ptr end does not match slot count";
+  for (std::uint32_t v = 1; v <= n; ++v) {
+    const std::uint32_t b = rp[v], e = rp[v + 1];
+    if (b >= e) return "row " + std::to_string(v) + " owns no sentinel slot";
+    if (col[e - 1] != 0) return "row " + std::to_string(v) + " does not end in a zero slot";
+    std::uint32_t prev = v;
+    bool zero_tail = false;
+    for (std::uint32_t s = b; s < e; ++s) {
+      const std::uint32_t w = col[s];
+      if (w == 0) {
+        zero_tail = true;
+        continue;
+      }
+      if (zero_tail) return "row " + std::to_string(v) + " has a nonzero after a zero slot";
+      if (w <= prev) return "row " + std::to_string(v) + " entries are not strictly ascending above the vertex";
+      if (w > n) return "row " + std::to_string(v) + " references vertex beyond n";
+      prev = w;
+    }
+  }
+  return "";
+}
+
+constexpr char kMagic[8] = {'Z', 'T', 'C', 'S', 'R', '1', '\0', '\0'};
+
 }  // namespace
 
 extern "C" {
@@ -326,6 +359,95 @@ void ktgg_csr_copy(const ktgg_csr* c, std::uint32_t* row_ptr, std::uint32_t* col
   if (original_ids) std::memcpy(original_ids, g->original_ids.data(), g->original_ids.size() * 8);
 }
 void ktgg_csr_free(ktgg_csr* c) { delete reinterpret_cast<Csr*>(c); }
+
+// ZTCSR1 cache (csr_cache.hpp:11-21, csr_cache.cpp:71-111): little-endian
+// magic | u32 n | u64 slots | row_ptr (n+2) x u32 | col_idx slots x u32.
+int ktgg_write_csr_cache(const char* path, const std::uint32_t* row_ptr, std::uint32_t n, const std::uint32_t* col,
+                         std::uint64_t slots) {
+  FILE* f = std::fopen(path, "wb");
+  if (!f) {
+    g_err = "cache write failed";
+    return KTGG_ERR_IO;
+  }
+  bool ok = std::fwrite(kMagic, 1, 8, f) == 8;
+  ok = ok && std::fwrite(&n, 4, 1, f) == 1;  // x86/ARM hosts are little-endian
+  ok = ok && std::fwrite(&slots, 8, 1, f) == 1;
+  ok = ok && std::fwrite(row_ptr, 4, n + std::size_t{2}, f) == n + std::size_t{2};
+  ok = ok && std::fwrite(col, 4, slots, f) == slots;
+  ok = (std::fclose(f) == 0) && ok;
+  if (!ok) {
+    g_err = "cache write failed";
+    return KTGG_ERR_IO;
+  }
+  return KTGG_OK;
+}
+
+int ktgg_read_csr_cache(const char* path, ktgg_csr** out) {
+  FILE* f = std::fopen(path, "rb");
+  if (!f) {
+    g_err = std::string("cannot open ") + path;
+    return KTGG_ERR_IO;
+  }
+  auto corrupt = [&](const std::string& m) {
+    std::fclose(f);
+    g_err = m;
+    return KTGG_ERR_CORRUPT_CACHE;
+  };
+  char magic[8];
+  if (std::fread(magic, 1, 8, f) != 8 || std::memcmp(magic, kMagic, 8) != 0) return corrupt("bad cache magic");
+  std::uint32_t n = 0;
+  std::uint64_t slots = 0;
+  if (std::fread(&n, 4, 1, f) != 1 || std::fread(&slots, 8, 1, f) != 1) return corrupt("truncated cache header");
+  if (n == 0 || slots < n || slots > 0xFFFFFFFFull) return corrupt("implausible cache dimensions");
+  Csr* c = nullptr;
+  try {
+    c = new Csr;
+    c->n = n;
+    c->row_ptr.resize(n + std::size_t{2});
+    if (std::fread(c->row_ptr.data(), 4, c->row_ptr.size(), f) != c->row_ptr.size()) {
+      delete c;
+      return corrupt("truncated cache payload");
+    }
+    if (c->row_ptr[n + 1] != slots) {
+      delete c;
+      return corrupt("row_ptr end does not match slot count");
+    }
+    c->col.resize(slots);
+    if (std::fread(c->col.data(), 4, slots, f) != slots) {
+      delete c;
+      return corrupt("truncated cache payload");
+    }
+    if (std::fgetc(f) != EOF) {
+      delete c;
+      return corrupt("trailing bytes after cache payload");
+    }
+  } catch (const std::bad_alloc&) {
+    delete c;
+    std::fclose(f);
+    g_err = "cache read: out of host memory";
+    return KTGG_ERR_OOM;
+  }
+  std::fclose(f);
+  const std::string bad = validate(n, c->row_ptr.data(), c->row_ptr.size(), c->col.data(), slots);
+  if (!bad.empty()) {
+    delete c;
+    g_err = "cache violates csr invariants: " + bad;
+    return KTGG_ERR_CORRUPT_CACHE;
+  }
+  c->original_ids.assign(n + std::size_t{1}, 0);
+  for (std::uint32_t v = 1; v <= n; ++v) c->original_ids[v] = v;
+  *out = reinterpret_cast<ktgg_csr*>(c);
+  return KTGG_OK;
+}
+
+// validate_csr restated; 0 if valid, else KTGG_ERR_INVALID_INPUT + message.
+int ktgg_validate_csr(const std::uint32_t* row_ptr, std::uint64_t rp_len, std::uint32_t n, const std::uint32_t* col,
+                      std::uint64_t slots) {
+  const std::string bad = validate(n, row_ptr, rp_len, col, slots);
+  if (bad.empty()) return KTGG_OK;
+  g_err = bad;
+  return KTGG_ERR_INVALID_INPUT;
+}
 
 // Closed-form merge work of one compute_supports pass over the live graph
 // (SURVEY.md §8(d)): L = sum_v d+(d+-1)/2 + d+ d-. Split into its two terms.

@@ -417,11 +417,98 @@ ktg_status engine_load(ktg_engine* e, const uint32_t* row_ptr, uint32_t n, const
   e->caller_stale = false;
   KTG_TRY(C.row_ptr.ensure((size_t)n + 2));
   KTG_TRY(C.col.ensure(slots + 4));
-  KTG_CUDA(cudaMemcpyAsync(C.row_ptr.p, row_ptr, ((size_t)n + 2) * 4, kind, e->stream));
-  KTG_CUDA(cudaMemcpyAsync(C.col.p, col, slots * 4, kind, e->stream));
+  if (row_ptr) KTG_CUDA(cudaMemcpyAsync(C.row_ptr.p, row_ptr, ((size_t)n + 2) * 4, kind, e->stream));
+  if (col) KTG_CUDA(cudaMemcpyAsync(C.col.p, col, slots * 4, kind, e->stream));
   KTG_TRY(prepare_layout(e, C, keep_pristine || e->reoriented));
   if (e->reoriented) KTG_TRY(build_working(e));
   return KTG_OK;
+}
+
+const char* kValidateMsg[6] = {"", " owns no sentinel slot", " does not end in a zero slot",
+                               " has a nonzero after a zero slot",
+                               " entries are not strictly ascending above the vertex",
+                               " references vertex beyond n"};
+
+// ZTCSR1 file -> HBM (csr_cache.cpp:80-111 semantics and messages), streamed
+// through two pinned staging buffers; invariants validated on the device.
+ktg_status load_cache(ktg_engine* e, const char* path) {
+  FILE* f = std::fopen(path, "rb");
+  if (!f) return fail(KTG_ERR_INVALID_PARAMETER, std::string("cannot open ") + path);
+  struct Closer {
+    FILE* f;
+    ~Closer() { std::fclose(f); }
+  } closer{f};
+  static const char kMagic[8] = {'Z', 'T', 'C', 'S', 'R', '1', '\0', '\0'};
+  char magic[8];
+  if (std::fread(magic, 1, 8, f) != 8 || std::memcmp(magic, kMagic, 8) != 0)
+    return fail(KTG_ERR_CORRUPT_CACHE, "bad cache magic");
+  uint32_t n = 0;
+  uint64_t slots = 0;
+  if (std::fread(&n, 4, 1, f) != 1 || std::fread(&slots, 8, 1, f) != 1)
+    return fail(KTG_ERR_CORRUPT_CACHE, "truncated cache header");
+  if (n == 0 || slots < n || slots > 0xFFFFFFFFull) return fail(KTG_ERR_CORRUPT_CACHE, "implausible cache dimensions");
+  Layout& C = e->cl;
+  KTG_TRY(C.row_ptr.ensure((size_t)n + 2));
+  KTG_TRY(C.col.ensure(slots + 4));
+  constexpr size_t kStage = size_t{32} << 20;
+  void* stage[2] = {nullptr, nullptr};
+  cudaEvent_t done[2] = {nullptr, nullptr};
+  auto release = [&]() {
+    for (int i = 0; i < 2; ++i) {
+      if (done[i]) cudaEventSynchronize(done[i]), cudaEventDestroy(done[i]);
+      if (stage[i]) cudaFreeHost(stage[i]);
+    }
+  };
+  ktg_status st = KTG_OK;
+  for (int i = 0; i < 2 && st == KTG_OK; ++i) {
+    if (cudaMallocHost(&stage[i], kStage) != cudaSuccess || cudaEventCreate(&done[i]) != cudaSuccess)
+      st = fail(KTG_ERR_OOM, "pinned staging allocation failed");
+  }
+  // stream row_ptr then col_idx through the staging buffers
+  struct Seg {
+    char* dst;
+    uint64_t bytes;
+  } segs[2] = {{reinterpret_cast<char*>(C.row_ptr.p), ((uint64_t)n + 2) * 4},
+               {reinterpret_cast<char*>(C.col.p), slots * 4}};
+  int buf = 0;
+  for (int sgi = 0; sgi < 2 && st == KTG_OK; ++sgi) {
+    for (uint64_t off = 0; off < segs[sgi].bytes && st == KTG_OK;) {
+      const size_t len = (size_t)std::min<uint64_t>(kStage, segs[sgi].bytes - off);
+      cudaEventSynchronize(done[buf]);
+      if (std::fread(stage[buf], 1, len, f) != len) {
+        st = fail(KTG_ERR_CORRUPT_CACHE, "truncated cache payload");
+        break;
+      }
+      if (cudaMemcpyAsync(segs[sgi].dst + off, stage[buf], len, cudaMemcpyHostToDevice, e->stream) != cudaSuccess ||
+          cudaEventRecord(done[buf], e->stream) != cudaSuccess)
+        st = fail(KTG_ERR_CUDA, "cache upload failed");
+      off += len;
+      buf ^= 1;
+    }
+  }
+  if (st == KTG_OK && std::fgetc(f) != EOF) st = fail(KTG_ERR_CORRUPT_CACHE, "trailing bytes after cache payload");
+  release();
+  if (st != KTG_OK) return st;
+  uint32_t head[2] = {0, 0}, last = 0;
+  KTG_CUDA(cudaMemcpy(head, C.row_ptr.p, 8, cudaMemcpyDeviceToHost));
+  KTG_CUDA(cudaMemcpy(&last, C.row_ptr.p + n + 1, 4, cudaMemcpyDeviceToHost));
+  if (last != slots) return fail(KTG_ERR_CORRUPT_CACHE, "row_ptr end does not match slot count");
+  if (head[0] != 0 || head[1] != 0)
+    return fail(KTG_ERR_CORRUPT_CACHE, "cache violates csr invariants: phantom vertex 0 must own no slots");
+  unsigned long long* d_first = nullptr;
+  KTG_CUDA(cudaMalloc(&d_first, 8));
+  unsigned long long first = ~0ull;
+  cudaMemcpy(d_first, &first, 8, cudaMemcpyHostToDevice);
+  k_validate_rows<<<e->prune_grid, kPruneThreads, 0, e->stream>>>(C.row_ptr.p, C.col.p, n, slots, d_first);
+  cudaError_t ve = cudaGetLastError();
+  if (ve == cudaSuccess) ve = cudaMemcpyAsync(&first, d_first, 8, cudaMemcpyDeviceToHost, e->stream);
+  if (ve == cudaSuccess) ve = cudaStreamSynchronize(e->stream);
+  cudaFree(d_first);
+  if (ve != cudaSuccess) return fail(KTG_ERR_CUDA, std::string("cache validation: ") + cudaGetErrorString(ve));
+  if (first != ~0ull)
+    return fail(KTG_ERR_CORRUPT_CACHE, "cache violates csr invariants: row " + std::to_string(first >> 3) +
+                                           kValidateMsg[first & 7]);
+  return engine_load(e, nullptr, n, nullptr, slots, cudaMemcpyDeviceToDevice, true, true);
 }
 
 // Caller-layout support buffer holding the current result.
@@ -845,6 +932,8 @@ ktg_status ktg_engine_load_device(ktg_engine* e, const uint32_t* d_row_ptr, uint
                                   const uint32_t* d_col_idx, uint64_t slots) {
   return engine_load(e, d_row_ptr, n, d_col_idx, slots, cudaMemcpyDeviceToDevice, true, true);
 }
+
+ktg_status ktg_engine_load_cache(ktg_engine* e, const char* path) { return load_cache(e, path); }
 
 ktg_status ktg_engine_reset(ktg_engine* e) { return reset(e); }
 

@@ -119,6 +119,49 @@ __global__ void k_init_deg(const uint32_t* __restrict__ row_ptr, const uint32_t*
   if ((threadIdx.x & 31) == 0 && live) atomicAdd(&st->live, live);
 }
 
+// validate_csr (csr.cpp:34-80) per-row checks on the device, warp per row:
+// first violation in reference order, packed row << 3 | code into *first
+// (atomicMin keeps the lowest row). Codes: 1 no sentinel slot, 2 no zero at
+// the row end, 3 nonzero after a zero, 4 not strictly ascending above the
+// vertex, 5 beyond n.
+__global__ void k_validate_rows(const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ col, uint32_t n,
+                                uint64_t slots, unsigned long long* first) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t v = warp + 1; v <= n; v += nwarps) {
+    const uint32_t b = row_ptr[v], e = row_ptr[v + 1];
+    uint32_t code = 0;
+    if (b >= e) code = 1;
+    else if (e > slots || col[e - 1] != 0) code = 2;  // e > slots: the reference reads past col (UB)
+    else {
+      uint32_t prev = v;      // value of the previous nonzero slot (or v)
+      bool zero_seen = false;
+      for (uint32_t off = b; off < e && code == 0; off += 32) {
+        const uint32_t x = off + lane;
+        const bool in = x < e;
+        const uint32_t w = in ? col[x] : 0u;
+        const unsigned zm = __ballot_sync(0xffffffffu, in && w == 0);
+        const bool zero_before = zero_seen || (zm & ((1u << lane) - 1u));
+        uint32_t pw = __shfl_up_sync(0xffffffffu, w, 1);
+        if (lane == 0) pw = prev;
+        // the previous slot is nonzero whenever this one is checked for order
+        uint32_t c = 0;
+        if (in && w != 0) {
+          if (zero_before) c = 3;
+          else if (w <= pw) c = 4;
+          else if (w > n) c = 5;
+        }
+        const unsigned bm = __ballot_sync(0xffffffffu, c != 0);
+        if (bm) code = __shfl_sync(0xffffffffu, c, __ffs(bm) - 1);
+        zero_seen = zero_seen || zm;
+        prev = __shfl_sync(0xffffffffu, w, 31);
+      }
+    }
+    if (lane == 0 && code) atomicMin(first, ((unsigned long long)v << 3) | code);
+  }
+}
+
 // Row containing the last slot of every chunk (fixed for the graph's life).
 __global__ void k_chunk_rows(const uint32_t* __restrict__ row_ptr, uint32_t n, uint64_t slots,
                              uint32_t nchunks, uint32_t* __restrict__ chunk_row) {

@@ -64,6 +64,8 @@ def _g():
         lib.ktgg_csr_copy.argtypes = [vp, vp, vp, vp]
         lib.ktgg_csr_free.argtypes = [vp]
         lib.ktgg_round_work.argtypes = [vp, ctypes.c_uint32, vp, ctypes.POINTER(_Work)]
+        lib.ktgg_write_csr_cache.argtypes = [ctypes.c_char_p, vp, ctypes.c_uint32, vp, ctypes.c_uint64]
+        lib.ktgg_read_csr_cache.argtypes = [ctypes.c_char_p, ctypes.POINTER(vp)]
         _configured = True
     return lib
 
@@ -76,6 +78,8 @@ def _raise(rc: int):
         raise errors.InvalidInputError(msg)
     if rc == 4:
         raise errors.EmptyGraphError(msg)
+    if rc == 5:
+        raise errors.CorruptCacheError(msg)
     if rc == 7:
         raise MemoryError(msg)
     raise errors.Error(msg)
@@ -176,6 +180,24 @@ def erdos_renyi(log_n: int, m: int, seed: int = 42) -> ZeroTerminatedCsr:
     if rc:
         _raise(rc)
     return _raw_to_csr(h)
+
+
+def write_csr_cache(g: ZeroTerminatedCsr, path: str) -> None:
+    """write_csr_cache (csr_cache.cpp:71-78): the ZTCSR1 binary layout."""
+    rc = _g().ktgg_write_csr_cache(path.encode(), _ptr(np.ascontiguousarray(g.row_ptr, np.uint32)), g.num_vertices,
+                                   _ptr(np.ascontiguousarray(g.col_idx, np.uint32)), g.total_slots())
+    if rc:
+        _raise(rc)
+
+
+def read_csr_cache(path: str) -> ZeroTerminatedCsr:
+    """read_csr_cache (csr_cache.cpp:80-111): raises CorruptCacheError with
+    the reference's messages."""
+    h = ctypes.c_void_p()
+    rc = _g().ktgg_read_csr_cache(path.encode(), ctypes.byref(h))
+    if rc:
+        _raise(rc)
+    return _csr_from_handle(h)
 
 
 def round_work(g: ZeroTerminatedCsr) -> dict:

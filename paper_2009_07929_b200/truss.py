@@ -184,6 +184,7 @@ def lib():
         L.ktg_engine_destroy.argtypes = [_vp]
         L.ktg_engine_load.argtypes = [_vp, _vp, _u32, _vp, _u64]
         L.ktg_engine_load_device.argtypes = [_vp, _vp, _u32, _vp, _u64]
+        L.ktg_engine_load_cache.argtypes = [_vp, ctypes.c_char_p]
         L.ktg_engine_reset.argtypes = [_vp]
         L.ktg_engine_run.argtypes = [_vp, _u32, _vp, _u32, P(_u32)]
         L.ktg_engine_support_pass.argtypes = [_vp, P(_u64)]
@@ -212,6 +213,8 @@ def _check(rc: int) -> None:
         raise errors.SupportOverflowError(int(L.ktg_last_error_slot()), msg)
     if rc == 3:
         raise errors.InvalidInputError(msg)
+    if rc == 4:
+        raise errors.CorruptCacheError(msg)
     if rc == 7:
         raise MemoryError(msg)
     raise errors.DeviceError(msg)
@@ -450,6 +453,16 @@ class Engine:
         self._keep["graph"] = graph
         rp, col = _u32arr(graph.row_ptr), _u32arr(graph.col_idx)
         _check(lib().ktg_engine_load(self._h, _p(rp), graph.num_vertices, _p(col), col.shape[0]))
+
+    def load_cache(self, path: str) -> None:
+        """ZTCSR1 file straight into HBM (validated on the device)."""
+        _check(lib().ktg_engine_load_cache(self._h, path.encode()))
+        import numpy as _np  # shape info for extract / read
+        with open(path, "rb") as f:
+            head = f.read(20)
+        n = int(_np.frombuffer(head[8:12], _np.uint32)[0])
+        slots = int(_np.frombuffer(head[12:20], _np.uint64)[0])
+        self.graph = ZeroTerminatedCsr(n, _np.zeros(0, _np.uint32), _np.zeros(slots, _np.uint32))
 
     def load_device(self, d_row_ptr: int, n: int, d_col: int, slots: int) -> None:
         _check(lib().ktg_engine_load_device(self._h, _vp(d_row_ptr), n, _vp(d_col), slots))
