@@ -46,6 +46,7 @@ typedef enum {
   KTG_ERR_SUPPORT_OVERFLOW = 2,  /* ktruss::SupportOverflowError; slot via ktg_last_error_slot() */
   KTG_ERR_INVALID_INPUT = 3,     /* ktruss::InvalidInputError                */
   KTG_ERR_CORRUPT_CACHE = 4,     /* ktruss::CorruptCacheError                */
+  KTG_ERR_EMPTY_GRAPH = 8,       /* ktruss::EmptyGraphError                  */
   KTG_ERR_CUDA = 5,              /* CUDA runtime / NCCL failure              */
   KTG_ERR_NO_DEVICE = 6,         /* no usable sm_100 device                  */
   KTG_ERR_OOM = 7                /* device or host allocation failed         */
@@ -189,6 +190,16 @@ ktg_status ktg_engine_load_device(ktg_engine* e, const uint32_t* d_row_ptr, uint
  * invariants validated on the device. Errors: KTG_ERR_CORRUPT_CACHE with the
  * reference's messages. */
 ktg_status ktg_engine_load_cache(ktg_engine* e, const char* path);
+/* canonicalize + build_csr on the device (edge_list.cpp:62-103, csr.cpp:10-32):
+ * m raw (label, label) pairs as u64 (host or device pointer) -> the
+ * reference's canonical zero-terminated CSR, loaded into the engine (CUB radix
+ * sorts + unique, binary-search relabel). Errors: KTG_ERR_EMPTY_GRAPH,
+ * KTG_ERR_INVALID_INPUT (> 2^32-1 slots / ids). */
+ktg_status ktg_engine_build_csr(ktg_engine* e, const uint64_t* pairs, uint64_t m, int pairs_on_device);
+ktg_status ktg_engine_csr_info(ktg_engine* e, uint32_t* n, uint64_t* slots);
+/* The loaded graph (pristine) to host; original_ids (n+1 u64, [0] unused)
+ * only for graphs built by ktg_engine_build_csr. Any pointer may be NULL. */
+ktg_status ktg_engine_read_csr(ktg_engine* e, uint32_t* row_ptr, uint32_t* col_idx, uint64_t* original_ids);
 /* Restores the pristine col_idx and zeroes both support buffers (async on
  * the engine stream). */
 ktg_status ktg_engine_reset(ktg_engine* e);

@@ -31,6 +31,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <functional>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -159,6 +160,8 @@ struct ktg_engine {
   DBuf<unsigned long long> keys, keys_sorted, ex_offs;
   DBuf<unsigned char> cub_tmp;
   DBuf<uint32_t> ex_out;
+  DBuf<unsigned long long> orig_ids;
+  bool has_orig_ids = false;
 
   unsigned long long* d_workL = nullptr;
   DevState* d_st = nullptr;
@@ -218,6 +221,7 @@ struct ktg_engine {
     keys.release();
     keys_sorted.release();
     ex_offs.release();
+    orig_ids.release();
     cub_tmp.release();
   }
 };
@@ -410,6 +414,7 @@ ktg_status engine_load(ktg_engine* e, const uint32_t* row_ptr, uint32_t n, const
   Layout& C = e->cl;
   C.ready = false;
   e->wl.ready = false;
+  if (row_ptr || col) e->has_orig_ids = false;
   C.n = n;
   C.slots = slots;
   C.has_payload = false;
@@ -934,6 +939,108 @@ ktg_status ktg_engine_load_device(ktg_engine* e, const uint32_t* d_row_ptr, uint
 }
 
 ktg_status ktg_engine_load_cache(ktg_engine* e, const char* path) { return load_cache(e, path); }
+
+ktg_status ktg_engine_build_csr(ktg_engine* e, const uint64_t* pairs, uint64_t m, int pairs_on_device) {
+  if (m == 0) return fail(KTG_ERR_EMPTY_GRAPH, "no edges survive canonicalization");
+  const cudaStream_t s = e->stream;
+  DBuf<unsigned long long> dpairs, lab, lab2, keys2;
+  auto cleanup = [&]() {
+    dpairs.release();
+    lab.release();
+    lab2.release();
+    keys2.release();
+  };
+  struct Guard {
+    std::function<void()> f;
+    ~Guard() { f(); }
+  } guard{cleanup};
+  const unsigned long long* src = reinterpret_cast<const unsigned long long*>(pairs);
+  if (!pairs_on_device) {
+    KTG_TRY(dpairs.ensure(2 * m));
+    KTG_CUDA(cudaMemcpyAsync(dpairs.p, pairs, 2 * m * 8, cudaMemcpyHostToDevice, s));
+    src = dpairs.p;
+  }
+  // 1. labels of non-loop pairs, sorted + unique
+  KTG_TRY(lab.ensure(2 * m));
+  KTG_TRY(lab2.ensure(2 * m));
+  k_pair_labels<<<8 * e->num_sms, 256, 0, s>>>(src, m, lab.p);
+  KTG_CUDA(cudaGetLastError());
+  size_t t1 = 0, t2 = 0;
+  KTG_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, t1, lab.p, lab2.p, (int64_t)(2 * m), 0, 64, s));
+  KTG_CUDA(cub::DeviceSelect::Unique(nullptr, t2, lab2.p, lab.p, e->d_workL, (int64_t)(2 * m), s));
+  KTG_TRY(e->cub_tmp.ensure(std::max(t1, t2)));
+  t1 = e->cub_tmp.cap;
+  KTG_CUDA(cub::DeviceRadixSort::SortKeys(e->cub_tmp.p, t1, lab.p, lab2.p, (int64_t)(2 * m), 0, 64, s));
+  t2 = e->cub_tmp.cap;
+  KTG_CUDA(cub::DeviceSelect::Unique(e->cub_tmp.p, t2, lab2.p, lab.p, e->d_workL, (int64_t)(2 * m), s));
+  unsigned long long nl = 0, last = 0;
+  KTG_CUDA(cudaMemcpyAsync(&nl, e->d_workL, 8, cudaMemcpyDeviceToHost, s));
+  KTG_CUDA(cudaStreamSynchronize(s));
+  if (nl) KTG_CUDA(cudaMemcpy(&last, lab.p + nl - 1, 8, cudaMemcpyDeviceToHost));
+  if (nl && last == ~0ull) --nl;  // drop the self-loop sentinel
+  if (nl == 0) return fail(KTG_ERR_EMPTY_GRAPH, "no edges survive canonicalization");
+  if (nl > 0xFFFFFFFEull) return fail(KTG_ERR_INVALID_INPUT, "vertex count exceeds 32-bit id space");
+  const uint32_t n = (uint32_t)nl;
+  // 2. relabel + orient -> (u, v) keys, sorted + unique
+  KTG_TRY(keys2.ensure(m));
+  k_pair_keys<<<8 * e->num_sms, 256, 0, s>>>(src, m, lab.p, n, lab2.p);
+  KTG_CUDA(cudaGetLastError());
+  t1 = e->cub_tmp.cap;
+  KTG_CUDA(cub::DeviceRadixSort::SortKeys(e->cub_tmp.p, t1, lab2.p, keys2.p, (int64_t)m, 0, 64, s));
+  t2 = e->cub_tmp.cap;
+  KTG_CUDA(cub::DeviceSelect::Unique(e->cub_tmp.p, t2, keys2.p, lab2.p, e->d_workL, (int64_t)m, s));
+  unsigned long long me = 0;
+  KTG_CUDA(cudaMemcpyAsync(&me, e->d_workL, 8, cudaMemcpyDeviceToHost, s));
+  KTG_CUDA(cudaStreamSynchronize(s));
+  if (me) KTG_CUDA(cudaMemcpy(&last, lab2.p + me - 1, 8, cudaMemcpyDeviceToHost));
+  if (me && last == ~0ull) --me;
+  if (me + n > 0xFFFFFFFFull) return fail(KTG_ERR_INVALID_INPUT, "graph exceeds 2^32-1 CSR slots");
+  // 3. rows: sizes (out-degree + sentinel), exclusive scan, fill
+  Layout& C = e->cl;
+  const uint64_t slots = me + n;
+  KTG_TRY(C.row_ptr.ensure((size_t)n + 2));
+  KTG_TRY(C.col.ensure(slots + 4));
+  KTG_TRY(e->cntw.ensure((size_t)n + 2));
+  KTG_TRY(e->sizes.ensure((size_t)n + 2));
+  KTG_CUDA(cudaMemsetAsync(e->cntw.p, 0, ((size_t)n + 2) * 4, s));
+  k_key_rows<<<8 * e->num_sms, 256, 0, s>>>(lab2.p, me, e->cntw.p);
+  k_row_sizes<<<4 * e->num_sms, 256, 0, s>>>(e->cntw.p, n, e->sizes.p);
+  KTG_CUDA(cudaGetLastError());
+  size_t t3 = 0;
+  KTG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t3, e->sizes.p, C.row_ptr.p, (int)(n + 2), s));
+  KTG_TRY(e->cub_tmp.ensure(t3));
+  t3 = e->cub_tmp.cap;
+  KTG_CUDA(cub::DeviceScan::ExclusiveSum(e->cub_tmp.p, t3, e->sizes.p, C.row_ptr.p, (int)(n + 2), s));
+  KTG_CUDA(cudaMemsetAsync(C.col.p, 0, slots * 4, s));
+  k_key_fill<<<8 * e->num_sms, 256, 0, s>>>(lab2.p, me, C.col.p);
+  KTG_CUDA(cudaGetLastError());
+  // original ids (labels) kept for ktg_engine_read_csr
+  KTG_TRY(e->orig_ids.ensure((size_t)n + 1));
+  KTG_CUDA(cudaMemsetAsync(e->orig_ids.p, 0, 8, s));
+  KTG_CUDA(cudaMemcpyAsync(e->orig_ids.p + 1, lab.p, (size_t)n * 8, cudaMemcpyDeviceToDevice, s));
+  e->has_orig_ids = true;
+  return engine_load(e, nullptr, n, nullptr, slots, cudaMemcpyDeviceToDevice, true, true);
+}
+
+ktg_status ktg_engine_csr_info(ktg_engine* e, uint32_t* n, uint64_t* slots) {
+  if (!e->cl.ready) return fail(KTG_ERR_INVALID_PARAMETER, "engine has no graph loaded");
+  *n = e->cl.n;
+  *slots = e->cl.slots;
+  return KTG_OK;
+}
+
+ktg_status ktg_engine_read_csr(ktg_engine* e, uint32_t* row_ptr, uint32_t* col_idx, uint64_t* original_ids) {
+  if (!e->cl.ready) return fail(KTG_ERR_INVALID_PARAMETER, "engine has no graph loaded");
+  Layout& C = e->cl;
+  const uint32_t* src = C.has_pristine ? C.col_p.p : C.col.p;  // the loaded (pristine) graph
+  if (row_ptr) KTG_CUDA(cudaMemcpy(row_ptr, C.row_ptr.p, ((size_t)C.n + 2) * 4, cudaMemcpyDeviceToHost));
+  if (col_idx) KTG_CUDA(cudaMemcpy(col_idx, src, C.slots * 4, cudaMemcpyDeviceToHost));
+  if (original_ids) {
+    if (!e->has_orig_ids) return fail(KTG_ERR_INVALID_PARAMETER, "graph was not built by ktg_engine_build_csr");
+    KTG_CUDA(cudaMemcpy(original_ids, e->orig_ids.p, ((size_t)C.n + 1) * 8, cudaMemcpyDeviceToHost));
+  }
+  return KTG_OK;
+}
 
 ktg_status ktg_engine_reset(ktg_engine* e) { return reset(e); }
 

@@ -850,6 +850,61 @@ k_prune_heavy(Graph g, int fused_reset) {
 }
 
 // ---------------------------------------------------------------------------
+// canonicalize + build_csr on the device
+// ---------------------------------------------------------------------------
+// Same result as edge_list.cpp:62-103 + csr.cpp:10-32: self-loops dropped,
+// labels relabelled 1..n by ascending original label, edges oriented u < v,
+// deduplicated, rows sorted; one zero sentinel per row. Self-loops / padding
+// become the ~0 sentinel key, which sorts last and is cut off.
+
+__global__ void k_pair_labels(const unsigned long long* __restrict__ pairs, uint64_t m,
+                              unsigned long long* __restrict__ labels) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
+    const unsigned long long a = pairs[2 * i], b = pairs[2 * i + 1];
+    const bool loop = a == b;
+    labels[2 * i] = loop ? ~0ull : a;
+    labels[2 * i + 1] = loop ? ~0ull : b;
+  }
+}
+
+__device__ __forceinline__ uint32_t label_rank(const unsigned long long* __restrict__ lab, uint32_t n,
+                                               unsigned long long x) {
+  uint32_t lo = 0, hi = n;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (lab[mid] < x) lo = mid + 1; else hi = mid;
+  }
+  return lo + 1;
+}
+
+__global__ void k_pair_keys(const unsigned long long* __restrict__ pairs, uint64_t m,
+                            const unsigned long long* __restrict__ lab, uint32_t n,
+                            unsigned long long* __restrict__ keys) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
+    const unsigned long long a = pairs[2 * i], b = pairs[2 * i + 1];
+    if (a == b) {
+      keys[i] = ~0ull;
+      continue;
+    }
+    const uint32_t u = label_rank(lab, n, a), v = label_rank(lab, n, b);
+    keys[i] = ((unsigned long long)min(u, v) << 32) | max(u, v);
+  }
+}
+
+__global__ void k_key_rows(const unsigned long long* __restrict__ keys, uint64_t m, uint32_t* __restrict__ cnt) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x)
+    atomicAdd(&cnt[(uint32_t)(keys[i] >> 32)], 1u);
+}
+
+// sorted unique keys -> col (slot = idx + u - 1, one sentinel per earlier row)
+__global__ void k_key_fill(const unsigned long long* __restrict__ keys, uint64_t m, uint32_t* __restrict__ col) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = keys[i];
+    col[i + (uint32_t)(k >> 32) - 1] = (uint32_t)k;
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Degree-ordered working layout
 // ---------------------------------------------------------------------------
 // Vertices are ranked by (undirected degree, id); every edge is oriented from

@@ -185,6 +185,9 @@ def lib():
         L.ktg_engine_load.argtypes = [_vp, _vp, _u32, _vp, _u64]
         L.ktg_engine_load_device.argtypes = [_vp, _vp, _u32, _vp, _u64]
         L.ktg_engine_load_cache.argtypes = [_vp, ctypes.c_char_p]
+        L.ktg_engine_build_csr.argtypes = [_vp, _vp, _u64, ctypes.c_int]
+        L.ktg_engine_csr_info.argtypes = [_vp, P(_u32), P(_u64)]
+        L.ktg_engine_read_csr.argtypes = [_vp, _vp, _vp, _vp]
         L.ktg_engine_reset.argtypes = [_vp]
         L.ktg_engine_run.argtypes = [_vp, _u32, _vp, _u32, P(_u32)]
         L.ktg_engine_support_pass.argtypes = [_vp, P(_u64)]
@@ -215,6 +218,8 @@ def _check(rc: int) -> None:
         raise errors.InvalidInputError(msg)
     if rc == 4:
         raise errors.CorruptCacheError(msg)
+    if rc == 8:
+        raise errors.EmptyGraphError(msg)
     if rc == 7:
         raise MemoryError(msg)
     raise errors.DeviceError(msg)
@@ -453,6 +458,32 @@ class Engine:
         self._keep["graph"] = graph
         rp, col = _u32arr(graph.row_ptr), _u32arr(graph.col_idx)
         _check(lib().ktg_engine_load(self._h, _p(rp), graph.num_vertices, _p(col), col.shape[0]))
+
+    def build_csr(self, pairs) -> ZeroTerminatedCsr:
+        """canonicalize + build_csr on the device from raw (label, label)
+        pairs; the result is loaded and also returned
+        (host copy with original_ids)."""
+        a = np.ascontiguousarray(np.asarray(pairs, dtype=np.uint64).reshape(-1, 2))
+        _check(lib().ktg_engine_build_csr(self._h, _p(a), a.shape[0], 0))
+        g = self.csr()
+        self.graph = g
+        self._keep["graph"] = g
+        return g
+
+    def csr(self) -> ZeroTerminatedCsr:
+        """The loaded (pristine) graph copied to the host."""
+        n, slots = _u32(), _u64()
+        _check(lib().ktg_engine_csr_info(self._h, ctypes.byref(n), ctypes.byref(slots)))
+        rp = np.empty(n.value + 2, np.uint32)
+        col = np.empty(slots.value, np.uint32)
+        ids = np.empty(n.value + 1, np.uint64)
+        rc = lib().ktg_engine_read_csr(self._h, _p(rp), _p(col), _p(ids))
+        if rc == 1:  # not built on device: no original ids
+            _check(lib().ktg_engine_read_csr(self._h, _p(rp), _p(col), None))
+            ids = None
+        else:
+            _check(rc)
+        return ZeroTerminatedCsr(int(n.value), rp, col, ids)
 
     def load_cache(self, path: str) -> None:
         """ZTCSR1 file straight into HBM (validated on the device)."""
