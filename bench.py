@@ -41,7 +41,18 @@ METRIC = "K-truss time-to-fixpoint (ms) & edges/sec at 1/2/4/8 B200; achieved HB
 # K_max of the pinned configs (reference-measured; also
 # asserted by tests/test_gpu_large.py) -- lets the reference arm skip its
 # ~200 s CPU kmax_search.
-KNOWN_KMAX = {(14, 16, 42): 79, (20, 16, 42): 304, (24, 16, 42): 935}
+KNOWN_KMAX = {(14, 16, 42): 79, (20, 16, 42): 304, (24, 16, 42): 935, ("er", 22, 16, 42): 3}
+
+
+def make_graph(args):
+    import paper_2009_07929_b200 as kt
+    if args.graph == "er":
+        return kt.erdos_renyi(args.scale, args.ef << args.scale, args.seed)
+    return kt.rmat(args.scale, args.ef, args.seed)
+
+
+def kmax_key(args):
+    return ("er", args.scale, args.ef, args.seed) if args.graph == "er" else (args.scale, args.ef, args.seed)
 
 
 def parse():
@@ -61,6 +72,8 @@ def parse():
                     help="sweep: K sweep 3..K_max (K split across ranks); fixpoint: one fixpoint per step "
                          "at --k (0 = K_max), edge-partitioned over NCCL across ranks")
     ap.add_argument("--k", type=int, default=0)
+    ap.add_argument("--graph", default="rmat", choices=["rmat", "er"],
+                    help="er: Erdős–Rényi with 2^scale vertices and ef*2^scale draws (SURVEY §8(d))")
     return ap.parse_args()
 
 
@@ -469,12 +482,12 @@ def run_fixpoint_mode(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     dev = torch.device("cuda", local)
     t0 = time.time()
-    g = kt.rmat(args.scale, args.ef, args.seed)
+    g = make_graph(args)
     gen_s = time.time() - t0
     n, slots, m = g.num_vertices, g.total_slots(), g.num_edges
     stream = torch.cuda.Stream()
     eng = kt.Engine(g, stream=stream.cuda_stream)
-    k = args.k or KNOWN_KMAX.get((args.scale, args.ef, args.seed)) or eng.kmax()
+    k = args.k or KNOWN_KMAX.get(kmax_key(args)) or eng.kmax()
     if world > 1:
         kd.engine_join(eng)
     eng.reset()
@@ -543,7 +556,8 @@ def run_fixpoint_mode(args):
             "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
-            "config": {"workload": f"rmat-s{args.scale}-ef{args.ef} K={k} fixpoint",
+            "config": {"workload": (f"er-2^{args.scale}-{args.ef}x K={k} fixpoint" if args.graph == "er" else
+                                    f"rmat-s{args.scale}-ef{args.ef} K={k} fixpoint"),
                        "n": n, "m": m, "slots": slots, "k": k, "rounds": len(hist),
                        "l2": "512 MiB memset between timed steps; inputs > L2" if slots * 4 > 126e6 else
                              "512 MiB memset between timed steps",

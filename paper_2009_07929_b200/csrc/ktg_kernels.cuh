@@ -72,22 +72,6 @@ __host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { re
 __device__ __forceinline__ uint32_t* cur_S(const Graph& g) { return g.st->parity ? g.S1 : g.S0; }
 __device__ __forceinline__ uint32_t* other_S(const Graph& g) { return g.st->parity ? g.S0 : g.S1; }
 
-__device__ __forceinline__ uint32_t lower_bound_g(const uint32_t* __restrict__ a, uint32_t lo, uint32_t hi,
-                                                  uint32_t key) {
-  while (lo < hi) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (__ldg(a + mid) < key) lo = mid + 1; else hi = mid;
-  }
-  return lo;
-}
-__device__ __forceinline__ uint32_t upper_bound_g(const uint32_t* __restrict__ a, uint32_t lo, uint32_t hi,
-                                                  uint32_t key) {
-  while (lo < hi) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (__ldg(a + mid) <= key) lo = mid + 1; else hi = mid;
-  }
-  return lo;
-}
 
 // ---------------------------------------------------------------------------
 // Setup kernels
@@ -298,20 +282,6 @@ __device__ __forceinline__ uint32_t lb_global(const uint32_t* __restrict__ a, ui
   return (uint32_t)(base - a) + (__ldg(base) < key);
 }
 
-// lower_bound in smem A[lo, hi)
-__device__ __forceinline__ uint32_t lower_bound_s(const uint32_t* A, uint32_t lo, uint32_t hi, uint32_t key) {
-  uint32_t len = hi - lo;
-  while (len > 0) {
-    const uint32_t half = len >> 1;
-    if (A[lo + half] < key) {
-      lo += half + 1;
-      len -= half + 1;
-    } else {
-      len = half;
-    }
-  }
-  return lo;
-}
 
 // Block-wide exclusive scan of one u32 per thread; returns the prefix, total
 // in *total. Uses red as scratch.

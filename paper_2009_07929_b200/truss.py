@@ -588,7 +588,9 @@ class Engine:
     def extract(self, cap: Optional[int] = None):
         """Survivors as a TrussResult-like (u, v, support) triple of u32
         columns (pinned host memory); .edges stacks them."""
-        cap = cap if cap is not None else max(1, self.graph.num_edges)
+        if cap is None:  # exact survivor count (synchronises)
+            self.sync()
+            cap = max(1, int(self.info()["live_edges"]))
         u, v, sup = _host_u32(cap), _host_u32(cap), _host_u32(cap)
         num = _u64()
         _check(lib().ktg_engine_extract(self._h, _p(u), _p(v), _p(sup), cap, ctypes.byref(num)))
