@@ -723,7 +723,10 @@ ktg_status overflow_error(ktg_engine* e) {
 
 ktg_status finish_info(ktg_engine* e) {
   float ms = 0;
-  KTG_CUDA(cudaEventElapsedTime(&ms, e->ev0, e->ev1));
+  if (cudaEventElapsedTime(&ms, e->ev0, e->ev1) != cudaSuccess) {  // no run recorded yet
+    cudaGetLastError();
+    ms = 0;
+  }
   e->info.iterations = e->h_st->iter;
   e->info.live_edges = e->h_st->live;
   e->info.triangles = e->h_st->last_triangles;
