@@ -99,6 +99,8 @@ uint64_t ktg_last_error_slot(void);
 /* Library / device probe: 1 if an sm_100 device is visible, else 0. */
 int ktg_device_available(void);
 const char* ktg_version(void);
+/* Slots per support-task chunk (the multi-GPU task partition unit). */
+uint32_t ktg_task_chunk(void);
 
 /* ---------------------------------------------------------------------- */
 /* Reference-shaped entry points (host buffers)                            */

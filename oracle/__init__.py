@@ -67,9 +67,10 @@ class _Port:
                                         threads)
         return int(t), S
 
-    def support_tasks(self, g, rank, world, chunk=1024):
+    def support_tasks(self, g, rank, world, chunk=512):
         """One rank's partial supports under the engine's task partition
-        (mirror of the device planner; see ktruss_oracle.c)."""
+        (mirror of the device planner; see ktruss_oracle.c). `chunk` must be
+        the engine's (ktg_task_chunk())."""
         S = np.zeros(g.total_slots(), np.uint32)
         t = self.L.orc_support_tasks(_p(_u32a(g.row_ptr)), g.num_vertices, _p(_u32a(g.col_idx)),
                                      g.total_slots(), chunk, rank, world, _p(S))

@@ -294,7 +294,9 @@ uint64_t orc_random_graph_raw(uint32_t n, double p, uint64_t seed, uint64_t* out
  * chunk q whose live part reaches chunk q' > q come first (q ascending, then
  * q'), then the diagonal tasks (q, q). Task t belongs to rank t % world. A
  * task processes the pivots of chunk q against the part of their a12 tails
- * lying in chunk q'. This restatement computes one rank's partial supports
+ * lying in chunk q'. Diagonal tasks run from the last chunk to the first
+ * (densest rows of the degree order first). This restatement computes one
+ * rank's partial supports
  * with the reference's merge (support.cpp:64-91) restricted to that tail
  * part. Returns the partial triangle count. S must be zero on entry. */
 static uint32_t row_of_slot(const uint32_t* row_ptr, uint32_t n, uint64_t s) {
@@ -348,9 +350,10 @@ uint64_t orc_support_tasks(const uint32_t* row_ptr, uint32_t n, const uint32_t* 
       for (uint64_t s = p_lo; s < e; ++s) tri += merge_range(row_ptr, col, s, a0, a1, S);
     }
   }
-  /* diagonal tasks */
-  for (uint64_t q = 0; q < Q; ++q, ++t) {
+  /* diagonal tasks, last chunk first */
+  for (uint64_t qi = 0; qi < Q; ++qi, ++t) {
     if (t % world != rank) continue;
+    const uint64_t q = Q - 1 - qi;
     const uint64_t p0 = q * chunk, p1 = (q + 1) * chunk < slots ? (q + 1) * chunk : slots;
     for (uint64_t s = p0; s < p1; ++s)
       if (col[s] != 0) tri += merge_range(row_ptr, col, s, s + 1, p1, S);

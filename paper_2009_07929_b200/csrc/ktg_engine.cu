@@ -890,6 +890,7 @@ void ktg_options_init(ktg_options* o) {
 const char* ktg_last_error(void) { return g_err.c_str(); }
 uint64_t ktg_last_error_slot(void) { return g_err_slot; }
 const char* ktg_version(void) { return "ktg 0.2 (sm_100a)"; }
+uint32_t ktg_task_chunk(void) { return (uint32_t)kChunk; }
 
 int ktg_device_available(void) {
   int count = 0;

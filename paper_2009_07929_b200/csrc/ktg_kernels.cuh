@@ -18,7 +18,7 @@
 
 namespace ktg {
 
-constexpr int kChunk = 1024;         // slots per staged chunk (P)
+constexpr int kChunk = 512;          // slots per staged chunk (P)
 constexpr int kSupportThreads = 256; // threads per support CTA
 constexpr int kPruneThreads = 256;
 constexpr int kHeavyRow = 2048;      // rows longer than this are pruned by a CTA
@@ -379,7 +379,7 @@ k_support_chunked(Graph g) {
       q = pr.x;
       q2 = pr.y;
     } else {
-      q = q2 = t - npairs;
+      q = q2 = g.nchunks - 1 - (t - npairs);  // dense (high-rank) chunks first
     }
     const bool diag = q == q2;
     const uint64_t a0 = (uint64_t)q2 * kChunk;

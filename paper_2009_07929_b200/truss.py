@@ -169,6 +169,7 @@ def lib():
         L.ktg_last_error_slot.restype = _u64
         L.ktg_version.restype = ctypes.c_char_p
         L.ktg_device_available.restype = ctypes.c_int
+        L.ktg_task_chunk.restype = _u32
         L.ktg_options_init.argtypes = [P(_Options)]
         L.ktg_compute_supports.argtypes = [_vp, _u32, _vp, _u64, _vp, _u64, P(_Options), P(_u64)]
         L.ktg_reset_supports.argtypes = [_vp, _u64]

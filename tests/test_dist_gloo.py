@@ -97,7 +97,7 @@ def _partitioned_fixpoint(rank, world):
         work = g.copy()
         hist = []
         while True:
-            _, S = P.support_tasks(work, rank, world)          # this rank's tasks
+            _, S = P.support_tasks(work, rank, world)          # this rank's tasks (engine chunking)
             t = torch.from_numpy(S.view(np.int32).copy())
             dist.all_reduce(t)                                  # exact integer sum
             S = t.numpy().view(np.uint32)

@@ -150,7 +150,7 @@ def test_rank_partials_match_oracle_task_partition(port):
             e.set_partition(r, world, allreduce=lambda *a: 0)
             e.reset()
             t = e.support_pass()
-            t_o, S_o = port.support_tasks(g, r, world)
+            t_o, S_o = port.support_tasks(g, r, world, chunk=kt.truss.lib().ktg_task_chunk())
             assert t == t_o and np.array_equal(e.read()[1], S_o), (world, r)
 
 
