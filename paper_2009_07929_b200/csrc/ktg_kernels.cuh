@@ -232,6 +232,8 @@ __global__ void __launch_bounds__(1024) k_plan_write(Graph g) {
 constexpr int kFilterBits = 1 << 15;     // membership filter over (value, row run)
 constexpr int kStrip = 256;              // flat elements a warp takes per grab (8 per lane)
 constexpr int kQueue = 64;               // per-warp queue of filter positives
+constexpr int kBuckets = kChunk / 4;     // position hash: kBuckets x 8 slots (load <= 0.5)
+constexpr int kStash = 32;               // overflow entries of full buckets
 
 struct SupportSmem {
   uint32_t A[kChunk];          // staged slots col[a0 .. a0+alen)
@@ -248,6 +250,11 @@ struct SupportSmem {
   uint32_t qk[kSupportThreads / 32][kQueue];   // queued (value, col position, pivot)
   uint32_t qpos[kSupportThreads / 32][kQueue];
   uint16_t qp[kSupportThreads / 32][kQueue];
+  __align__(16) uint32_t hkey[kBuckets][8];   // staged value (0 = empty)
+  __align__(16) uint32_t hmeta[kBuckets][8];  // row-run end << 16 | position
+  uint32_t hcnt[kBuckets];
+  uint32_t skey[kStash], smeta[kStash];
+  uint32_t nstash;
   uint32_t red[kSupportThreads / 32];
   uint32_t task;
   uint32_t next;               // flat work counter of the current task
@@ -255,6 +262,39 @@ struct SupportSmem {
 
 __device__ __forceinline__ uint32_t filt_hash(uint32_t k, uint32_t te) {
   return ((k ^ (te * 0x85EBCA6Bu)) * 2654435761u) >> (32 - 15);
+}
+
+__device__ __forceinline__ uint32_t bucket_of(uint32_t k, uint32_t te) {
+  return (((k ^ (te * 0x85EBCA6Bu)) * 2654435761u) >> 16) % kBuckets;
+}
+
+// Position of value k in the row run ending at te, at or after tb; kChunk if
+// absent. One bucket read (2 x 128-bit); only an overflowed bucket consults
+// the stash.
+template <typename Smem>
+__device__ __forceinline__ uint32_t hash_find(const Smem& s, uint32_t k, uint32_t tb, uint32_t te) {
+  const uint32_t b = bucket_of(k, te);
+  const uint4 k0 = *reinterpret_cast<const uint4*>(&s.hkey[b][0]);
+  const uint4 k1 = *reinterpret_cast<const uint4*>(&s.hkey[b][4]);
+  uint32_t m = (k0.x == k) | ((k0.y == k) << 1) | ((k0.z == k) << 2) | ((k0.w == k) << 3) |
+               ((k1.x == k) << 4) | ((k1.y == k) << 5) | ((k1.z == k) << 6) | ((k1.w == k) << 7);
+  while (m) {
+    const int i = __ffs(m) - 1;
+    m &= m - 1;
+    const uint32_t meta = s.hmeta[b][i];
+    const uint32_t pos = meta & 0xffffu;
+    if ((meta >> 16) == te && pos >= tb) return pos;
+  }
+  if (s.hcnt[b] <= 8) return kChunk;
+  const uint32_t ns = min(s.nstash, (uint32_t)kStash);
+  for (uint32_t i = 0; i < ns; ++i) {
+    if (s.skey[i] == k) {
+      const uint32_t meta = s.smeta[i];
+      const uint32_t pos = meta & 0xffffu;
+      if ((meta >> 16) == te && pos >= tb) return pos;
+    }
+  }
+  return kChunk;
 }
 
 // Branchless lower_bound over a sorted run a[0, n) (n >= 1 not required):
@@ -319,8 +359,14 @@ __device__ __forceinline__ bool confirm(SupportSmem& s, uint32_t* __restrict__ S
                                         uint32_t k, uint32_t pos, uint32_t p) {
   const uint32_t te = s.te[p] & 0x7fffu;
   const uint32_t tb = diag ? p + 1 : 0;
-  const uint32_t x = tb + lb_smem(s.A + tb, te - tb, k);
-  if (x < te && s.A[x] == k) {
+  uint32_t x;
+  if (s.nstash <= (uint32_t)kStash) {
+    x = hash_find(s, k, tb, te);
+  } else {
+    x = tb + lb_smem(s.A + tb, te - tb, k);
+    if (!(x < te && s.A[x] == k)) x = kChunk;
+  }
+  if (x < (uint32_t)kChunk) {
     atomicAdd(&s.cntA[x], 1u);
     atomicAdd(&S[pos], 1u);
     atomicAdd(&cntPiv[p], 1u);
@@ -339,7 +385,8 @@ __device__ __forceinline__ bool confirm(SupportSmem& s, uint32_t* __restrict__ S
 //   3. flatten all pivots' work with a prefix sum; warps grab strips of it
 //      dynamically; each lane caches its pivot's descriptor in registers;
 //      SCAN elements that pass the filter (~hits + 1.5% false positives) are
-//      queued per warp and confirmed 32 at a time by a full-warp binary search;
+//      queued per warp and confirmed 32 at a time by a (value, row-run) bucket
+//      hash that returns the tail position in one bucket read;
 //   4. a match (i,j,k) adds 1 to S[slot(i,k)] (smem), S[slot(j,k)] (global
 //      red.add) and the pivot's count (smem); smem counts are flushed once.
 // Semantically each pivot slot gets exactly intersect_tails' matches
@@ -365,9 +412,15 @@ k_support_chunked(Graph g) {
     if (tid == 0) {
       s.task = atomicAdd(&g.st->task_next, 1u);
       s.next = 0;
+      s.nstash = 0;
     }
 #pragma unroll
     for (int e = 0; e < FPT; ++e) s.filt[tid * FPT + e] = 0;
+    for (uint32_t b = tid; b < (uint32_t)kBuckets; b += kSupportThreads) {
+      s.hcnt[b] = 0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) s.hkey[b][e] = 0;
+    }
     __syncthreads();
     const uint32_t local = s.task;
     const uint64_t t64 = (uint64_t)local * g.world + g.rank;
@@ -426,6 +479,19 @@ k_support_chunked(Graph g) {
         if (v != 0) {
           const uint32_t h = filt_hash(v, cur);
           atomicOr(&s.filt[h >> 5], 1u << (h & 31));
+          const uint32_t b = bucket_of(v, cur);
+          const uint32_t at = atomicAdd(&s.hcnt[b], 1u);
+          const uint32_t meta = (cur << 16) | x;
+          if (at < 8) {
+            s.hkey[b][at] = v;
+            s.hmeta[b][at] = meta;
+          } else {
+            const uint32_t z = atomicAdd(&s.nstash, 1u);
+            if (z < kStash) {
+              s.skey[z] = v;
+              s.smeta[z] = meta;
+            }
+          }
         }
       }
     }
