@@ -230,7 +230,7 @@ __global__ void __launch_bounds__(1024) k_plan_write(Graph g) {
 // Support kernel
 // ---------------------------------------------------------------------------
 constexpr int kFilterBits = 1 << 15;     // membership filter over (value, row run)
-constexpr int kStrip = 256;              // flat elements a warp takes per grab (8 per lane)
+constexpr int kStrip = 512;              // flat elements a warp takes per grab (16 per lane)
 constexpr int kQueue = 64;               // per-warp queue of filter positives
 constexpr int kBuckets = kChunk / 4;     // position hash: kBuckets x 8 slots (load <= 0.5)
 constexpr int kStash = 32;               // overflow entries of full buckets
