@@ -73,9 +73,16 @@ enum {
                                        live edges and triangles (extra kernels) */
   KTG_FLAG_TIME_SUPPORT = 1u << 3,  /* host loop; CUDA events around every
                                        support launch (ktg_round_work.support_ms) */
-  KTG_FLAG_LABEL_ORDER = 1u << 4    /* run the fixpoint on the caller's (label-
+  KTG_FLAG_LABEL_ORDER = 1u << 4,   /* run the fixpoint on the caller's (label-
                                        ordered) CSR instead of the internal
                                        degree-ordered working copy */
+  KTG_FLAG_RECOMPUTE = 1u << 5      /* recompute every round's supports from
+                                       scratch (reset + computeSupports,
+                                       truss.cpp:44-46) instead of carrying
+                                       them: the default working-layout run
+                                       decrements the supports of triangles
+                                       that lose an edge whenever that is
+                                       cheaper (same S, same rounds) */
 };
 
 typedef struct {

@@ -163,6 +163,18 @@ struct ktg_engine {
   DBuf<unsigned long long> orig_ids;
   bool has_orig_ids = false;
 
+  // incremental rounds: symmetric adjacency of the working layout (+ pristine
+  // copies), per-edge dead flags and positions, delta task queue
+  DBuf<unsigned long long> sym_ptr, sym_sizes;
+  DBuf<uint32_t> sym_nbr, sym_eid, sym_nbr_p, sym_eid_p, sym_deg, sym_deg_p, pos_of, pos_of_p, erow, qsym,
+      qrow, fq0, fq1, sym_heavy;
+  DBuf<uint8_t> dead, rdirty, sdirty;
+  DBuf<uint4> rq;
+  uint64_t sym_entries = 0, rq_cap = 0;
+  bool sym_ready = false;
+  bool inc_active = false;    // the current fixpoint carries supports
+  uint32_t delta_ratio16 = 1;  // carry when delta_cost <= keep_cost / 16 (s20 sweep calibration, scripts/ratio_scan.py)
+
   unsigned long long* d_workL = nullptr;
   DevState* d_st = nullptr;
   unsigned long long* d_hist = nullptr;
@@ -212,6 +224,26 @@ struct ktg_engine {
     return g;
   }
 
+  Sym sym() {
+    Sym y;
+    y.ptr = sym_ptr.p;
+    y.nbr = sym_nbr.p;
+    y.eid = sym_eid.p;
+    y.deg = sym_deg.p;
+    y.dead = dead.p;
+    y.rdirty = rdirty.p;
+    y.sdirty = sdirty.p;
+    y.qsym = qsym.p;
+    y.qrow = qrow.p;
+    y.heavy = sym_heavy.p;
+    y.pos_of = pos_of.p;
+    y.erow = erow.p;
+    y.fq0 = fq0.p;
+    y.fq1 = fq1.p;
+    y.rq = rq.p;
+    return y;
+  }
+
   void free_all() {
     if (exec) cudaGraphExecDestroy(exec);
     exec = nullptr;
@@ -223,6 +255,16 @@ struct ktg_engine {
     ex_offs.release();
     orig_ids.release();
     cub_tmp.release();
+    for (DBuf<uint32_t>* b : {&sym_nbr, &sym_eid, &sym_nbr_p, &sym_eid_p, &sym_deg, &sym_deg_p, &pos_of, &pos_of_p,
+                              &erow, &qsym, &qrow, &fq0, &fq1, &sym_heavy})
+      b->release();
+    sym_ptr.release();
+    sym_sizes.release();
+    dead.release();
+    rdirty.release();
+    sdirty.release();
+    rq.release();
+    sym_ready = false;
   }
 };
 
@@ -254,6 +296,7 @@ ktg_status engine_init(const ktg_options* opt, ktg_engine* e) {
                                        " is not sm_100 (this build targets sm_100a only)");
   e->num_sms = prop.multiProcessorCount;
   if (const char* r = getenv("KTG_SCAN_RATIO")) e->scan_ratio = (uint32_t)std::max(1, atoi(r));
+  if (const char* r = getenv("KTG_DELTA_RATIO")) e->delta_ratio16 = (uint32_t)std::max(0.0, 16.0 * atof(r));
   if (e->opt.stream) {
     e->stream = static_cast<cudaStream_t>(e->opt.stream);
   } else {
@@ -402,6 +445,91 @@ ktg_status build_working(ktg_engine* e) {
   return prepare_layout(e, W, true);
 }
 
+// Symmetric adjacency of the (pristine) working layout for incremental
+// rounds: row v = sorted in-neighbours ++ out-neighbours (working row v), each
+// with the edge id; pos_of; pristine copies; the delta queue.
+ktg_status build_sym(ktg_engine* e) {
+  Layout& W = e->wl;
+  const uint32_t n = W.n;
+  const uint64_t m = W.live_pristine;
+  const size_t nb = (size_t)n + 2;
+  const cudaStream_t s = e->stream;
+  e->sym_ready = false;
+  if (n > 0x7fffffffu) return KTG_OK;  // col marks need the top bit
+  e->sym_entries = 2 * m;
+  KTG_TRY(e->sym_ptr.ensure(nb));
+  KTG_TRY(e->sym_sizes.ensure(5 * nb));
+  KTG_TRY(e->sym_nbr.ensure(2 * m));
+  KTG_TRY(e->sym_eid.ensure(2 * m));
+  KTG_TRY(e->sym_nbr_p.ensure(2 * m));
+  KTG_TRY(e->sym_eid_p.ensure(2 * m));
+  KTG_TRY(e->sym_deg.ensure(nb));
+  KTG_TRY(e->sym_deg_p.ensure(nb));
+  KTG_TRY(e->rdirty.ensure(nb));
+  KTG_TRY(e->sdirty.ensure(nb));
+  KTG_TRY(e->qsym.ensure(nb));
+  KTG_TRY(e->qrow.ensure(nb));
+  KTG_TRY(e->sym_heavy.ensure(nb));
+  KTG_TRY(e->fq0.ensure(m));
+  KTG_TRY(e->fq1.ensure(m));
+  KTG_TRY(e->pos_of.ensure(e->cl.slots));
+  KTG_TRY(e->pos_of_p.ensure(e->cl.slots));
+  KTG_TRY(e->erow.ensure(e->cl.slots));
+  KTG_TRY(e->dead.ensure(e->cl.slots));
+  KTG_TRY(e->din.ensure(nb));
+  KTG_TRY(e->keys.ensure(std::max<uint64_t>(m, n)));
+  KTG_TRY(e->keys_sorted.ensure(std::max<uint64_t>(m, n)));
+  KTG_TRY(e->vals.ensure(m));
+  KTG_TRY(e->vals_sorted.ensure(m));
+  Graph g = e->graph_of(W);
+  unsigned long long* sz = e->sym_sizes.p;  // [tot | din | dout | inoff | outoff] x nb
+  KTG_CUDA(cudaMemsetAsync(e->din.p, 0, nb * 4, s));
+  k_work_din<<<e->prune_grid, kPruneThreads, 0, s>>>(g, e->din.p);
+  k_u32_to_u64<<<4 * e->num_sms, 256, 0, s>>>(e->din.p, (uint32_t)nb, sz + nb);
+  k_u32_to_u64<<<4 * e->num_sms, 256, 0, s>>>(W.deg.p, (uint32_t)nb, sz + 2 * nb);
+  KTG_CUDA(cudaGetLastError());
+  size_t tmp = 0, tmp2 = 0;
+  KTG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, sz, e->sym_ptr.p, (int)nb, s));
+  uint32_t B = 1;
+  while ((1ull << B) <= n) ++B;
+  KTG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp2, e->keys.p, e->keys_sorted.p, e->vals.p,
+                                           e->vals_sorted.p, (int64_t)m, 0, 2 * B, s));
+  KTG_TRY(e->cub_tmp.ensure(std::max(tmp, tmp2)));
+  // tot = din + dout (one add kernel via the scan of the two halves)
+  k_add_u64<<<4 * e->num_sms, 256, 0, s>>>(sz + nb, sz + 2 * nb, (uint32_t)nb, sz);
+  tmp = e->cub_tmp.cap;
+  KTG_CUDA(cub::DeviceScan::ExclusiveSum(e->cub_tmp.p, tmp, sz, e->sym_ptr.p, (int)nb, s));
+  tmp = e->cub_tmp.cap;
+  KTG_CUDA(cub::DeviceScan::ExclusiveSum(e->cub_tmp.p, tmp, sz + nb, sz + 3 * nb, (int)nb, s));
+  tmp = e->cub_tmp.cap;
+  KTG_CUDA(cub::DeviceScan::ExclusiveSum(e->cub_tmp.p, tmp, sz + 2 * nb, sz + 4 * nb, (int)nb, s));
+  k_sym_in_keys<<<e->prune_grid, kPruneThreads, 0, s>>>(g, B, e->keys.p, e->vals.p, sz + 4 * nb);
+  KTG_CUDA(cudaGetLastError());
+  tmp = e->cub_tmp.cap;
+  KTG_CUDA(cub::DeviceRadixSort::SortPairs(e->cub_tmp.p, tmp, e->keys.p, e->keys_sorted.p, e->vals.p,
+                                           e->vals_sorted.p, (int64_t)m, 0, 2 * B, s));
+  Sym y = e->sym();
+  k_sym_fill<<<e->prune_grid, kPruneThreads, 0, s>>>(g, B, e->keys_sorted.p, e->vals_sorted.p, sz + 3 * nb,
+                                                     e->din.p, y);
+  KTG_CUDA(cudaMemsetAsync(e->d_workL, 0, 8, s));
+  k_sym_pos<<<e->prune_grid, kPruneThreads, 0, s>>>(g, y, e->d_workL);
+  KTG_CUDA(cudaGetLastError());
+  KTG_CUDA(cudaMemcpyAsync(e->sym_nbr_p.p, e->sym_nbr.p, 2 * m * 4, cudaMemcpyDeviceToDevice, s));
+  KTG_CUDA(cudaMemcpyAsync(e->sym_eid_p.p, e->sym_eid.p, 2 * m * 4, cudaMemcpyDeviceToDevice, s));
+  KTG_CUDA(cudaMemcpyAsync(e->sym_deg_p.p, e->sym_deg.p, nb * 4, cudaMemcpyDeviceToDevice, s));
+  KTG_CUDA(cudaMemcpyAsync(e->pos_of_p.p, e->pos_of.p, e->cl.slots * 4, cudaMemcpyDeviceToDevice, s));
+  KTG_CUDA(cudaMemsetAsync(e->dead.p, 0, e->cl.slots, s));
+  KTG_CUDA(cudaMemsetAsync(e->rdirty.p, 0, nb, s));
+  KTG_CUDA(cudaMemsetAsync(e->sdirty.p, 0, nb, s));
+  unsigned long long cap = 0;
+  KTG_CUDA(cudaMemcpyAsync(&cap, e->d_workL, 8, cudaMemcpyDeviceToHost, s));
+  KTG_CUDA(cudaStreamSynchronize(s));
+  e->rq_cap = cap;
+  KTG_TRY(e->rq.ensure(cap));
+  e->sym_ready = true;
+  return KTG_OK;
+}
+
 // Uploads (host or device source) into the caller layout; builds the working
 // layout unless the label order is requested. Buffers are reused when the
 // new graph fits (the host-buffer entry points keep one cached engine per
@@ -425,7 +553,10 @@ ktg_status engine_load(ktg_engine* e, const uint32_t* row_ptr, uint32_t n, const
   if (row_ptr) KTG_CUDA(cudaMemcpyAsync(C.row_ptr.p, row_ptr, ((size_t)n + 2) * 4, kind, e->stream));
   if (col) KTG_CUDA(cudaMemcpyAsync(C.col.p, col, slots * 4, kind, e->stream));
   KTG_TRY(prepare_layout(e, C, keep_pristine || e->reoriented));
-  if (e->reoriented) KTG_TRY(build_working(e));
+  if (e->reoriented) {
+    KTG_TRY(build_working(e));
+    if (!flag(e, KTG_FLAG_RECOMPUTE)) KTG_TRY(build_sym(e));
+  }
   return KTG_OK;
 }
 
@@ -529,6 +660,20 @@ ktg_status publish(ktg_engine* e) {
   if (!e->reoriented || !e->caller_stale) return KTG_OK;
   Layout& C = e->cl;
   const cudaStream_t s = e->stream;
+  if (e->sym_ready && e->inc_active) {
+    // every caller slot knows its fate (dead flag) and its working slot:
+    // one stable compaction pass from the pristine rows
+    Graph g = e->graph_of(C);
+    k_clear_heavy<<<1, 1, 0, s>>>(e->d_st);
+    k_publish_inc<0><<<e->prune_grid, kPruneThreads, 0, s>>>(g, C.col_p.p, C.deg_p.p, e->dead.p, e->pos_of.p,
+                                                            e->wl.S0.p);
+    k_publish_inc<1><<<e->heavy_grid, kPruneThreads, 0, s>>>(g, C.col_p.p, C.deg_p.p, e->dead.p, e->pos_of.p,
+                                                            e->wl.S0.p);
+    k_clear_heavy<<<1, 1, 0, s>>>(e->d_st);
+    KTG_CUDA(cudaGetLastError());
+    e->caller_stale = false;
+    return KTG_OK;
+  }
   KTG_CUDA(cudaMemsetAsync(C.col.p, 0, C.slots * 4, s));
   KTG_CUDA(cudaMemsetAsync(C.S0.p, 0, C.slots * 4, s));
   k_scatter_live<<<e->prune_grid, kPruneThreads, 0, s>>>(e->graph_of(e->wl), C.col_p.p, C.col.p, C.S0.p, 0);
@@ -560,6 +705,24 @@ ktg_status enqueue_round(ktg_engine* e, bool graph_mode, cudaGraphConditionalHan
     k_support_chunked<<<e->support_grid, kSupportThreads, e->support_smem, s>>>(g);
   }
   if (sup1) KTG_CUDA(cudaEventRecord(sup1, s));
+  if (e->inc_active) {
+    // mark -> [carry: delta] -> compact rows (col, ids, carried S) -> compact
+    // symmetric rows -> control (next round's mode, while condition)
+    const Sym y = e->sym();
+    k_mark<<<e->prune_grid, kPruneThreads, 0, s>>>(g, y);
+    k_mark_frontier<<<e->prune_grid, kPruneThreads, 0, s>>>(g, y);
+    k_decide<<<1, 1, 0, s>>>(e->d_st);
+    k_queues<<<4 * e->num_sms, 256, 0, s>>>(g, y);
+    k_delta<<<e->prune_grid, kPruneThreads, 0, s>>>(g, y);
+    k_inc_rows<0><<<e->prune_grid, kPruneThreads, 0, s>>>(g, y);
+    k_inc_rows<1><<<e->heavy_grid, kPruneThreads, 0, s>>>(g, y);
+    k_inc_sym<0><<<e->prune_grid, kPruneThreads, 0, s>>>(g, y);
+    k_inc_sym<1><<<e->heavy_grid, kPruneThreads, 0, s>>>(g, y);
+    k_inc_zero<<<4 * e->num_sms, 256, 0, s>>>(g);
+    k_control_inc<<<1, 1, 0, s>>>(e->d_st, e->d_hist, handle, graph_mode ? 1 : 0);
+    KTG_CUDA(cudaGetLastError());
+    return KTG_OK;
+  }
   if (e->opt.width_bits == 16) k_check16<<<4 * e->num_sms, 256, 0, s>>>(g);
   KTG_CUDA(cudaGetLastError());
   if (!graph_mode && (e->nccl || (e->world > 1 && e->allreduce))) {
@@ -587,7 +750,7 @@ ktg_status build_graph(ktg_engine* e) {
   const void* key[4] = {L.col.p, L.id.p, L.S0.p, L.pairs.p};
   const uint64_t key2[4] = {L.slots, L.n, (uint64_t)(flag(e, KTG_FLAG_NAIVE_SUPPORT) ? 1 : 0),
                             (uint64_t)e->opt.width_bits | ((uint64_t)e->reoriented << 8) |
-                                ((uint64_t)e->scan_ratio << 16)};
+                                ((uint64_t)e->scan_ratio << 16) | ((uint64_t)e->inc_active << 48)};
   if (e->exec && std::equal(key, key + 4, e->exec_key) && std::equal(key2, key2 + 4, e->exec_key2))
     return KTG_OK;
   if (e->exec) cudaGraphExecDestroy(e->exec);
@@ -629,8 +792,24 @@ ktg_status build_graph(ktg_engine* e) {
 // Prepares the device state for a fixpoint at k. parity < 0 switches to the
 // other support buffer on the device (it is all zero whenever the previous
 // run converged, see k_prune_light), parity >= 0 selects it explicitly.
+// Incremental rounds (supports carried across rounds when cheaper) run on the
+// working layout of a single-rank engine with 32-bit widths and no observer;
+// KTG_FLAG_RECOMPUTE keeps the paper's full pass every round.
+bool inc_eligible(const ktg_engine* e) {
+  return e->reoriented && e->sym_ready && !flag(e, KTG_FLAG_RECOMPUTE) && !flag(e, KTG_FLAG_NAIVE_SUPPORT) &&
+         e->opt.width_bits == 32 && e->opt.observer == nullptr && e->world == 1 && e->nccl == nullptr &&
+         e->allreduce == nullptr;
+}
+
 ktg_status begin_run(ktg_engine* e, uint32_t k, int parity) {
-  k_begin<<<1, 1, 0, e->stream>>>(e->d_st, k >= 2 ? k - 2 : 0, e->opt.width_bits == 16 ? 1 : 0, parity);
+  e->inc_active = inc_eligible(e);
+  if (e->inc_active) {
+    // one support buffer; round 0 is a full pass into a zeroed S0
+    KTG_CUDA(cudaMemsetAsync(e->wl.S0.p, 0, e->wl.slots * 4, e->stream));
+    parity = 0;
+  }
+  k_begin<<<1, 1, 0, e->stream>>>(e->d_st, k >= 2 ? k - 2 : 0, e->opt.width_bits == 16 ? 1 : 0, parity,
+                                  e->inc_active ? 1u : 0u, e->delta_ratio16);
   KTG_CUDA(cudaGetLastError());
   return KTG_OK;
 }
@@ -653,6 +832,15 @@ ktg_status collect_work(ktg_engine* e, ktg_round_work* w) {
   return KTG_OK;
 }
 
+// After a carried run: T of the converged graph from its supports.
+ktg_status inc_finish(ktg_engine* e) {
+  if (!e->inc_active) return KTG_OK;
+  k_inc_triangles<<<4 * e->num_sms, 256, 0, e->stream>>>(e->graph_of(e->wl));
+  k_inc_triangles_done<<<1, 1, 0, e->stream>>>(e->d_st);
+  KTG_CUDA(cudaGetLastError());
+  return KTG_OK;
+}
+
 // The fixpoint on the active layout. Expects begin_run() already enqueued.
 // Publishes the caller layout afterwards (enqueued).
 ktg_status run_loop(ktg_engine* e, bool want_sync) {
@@ -667,6 +855,7 @@ ktg_status run_loop(ktg_engine* e, bool want_sync) {
   if (!host_loop) {
     KTG_TRY(build_graph(e));
     KTG_CUDA(cudaGraphLaunch(e->exec, e->stream));
+    KTG_TRY(inc_finish(e));
     KTG_TRY(publish(e));
     KTG_CUDA(cudaEventRecord(e->ev1, e->stream));
     if (!want_sync) return KTG_OK;
@@ -682,7 +871,7 @@ ktg_status run_loop(ktg_engine* e, bool want_sync) {
     // Host loop keeps S semantics of the reference: the round's buffer is
     // zeroed up front (reset_supports), prune leaves S untouched.
     uint32_t* Sc = e->h_st->parity ? L.S1.p : L.S0.p;
-    KTG_CUDA(cudaMemsetAsync(Sc, 0, L.slots * 4, e->stream));
+    if (!e->inc_active) KTG_CUDA(cudaMemsetAsync(Sc, 0, L.slots * 4, e->stream));
     ktg_round_work w{};
     if (flag(e, KTG_FLAG_COLLECT_WORK)) KTG_TRY(collect_work(e, &w));
     KTG_TRY(enqueue_round(e, false, 0, timing ? e->evs0 : nullptr, timing ? e->evs1 : nullptr));
@@ -707,6 +896,7 @@ ktg_status run_loop(ktg_engine* e, bool want_sync) {
     }
     if (removed == 0 || e->h_st->error) break;
   }
+  KTG_TRY(inc_finish(e));
   KTG_TRY(publish(e));
   KTG_CUDA(cudaEventRecord(e->ev1, e->stream));
   return read_state(e);
@@ -749,7 +939,8 @@ ktg_status copy_hist(ktg_engine* e, uint64_t* hist, uint32_t cap, uint32_t* iter
 ktg_status support_pass(ktg_engine* e, int parity, uint64_t* triangles, bool max_support, bool add_to_caller) {
   Layout& L = e->act();
   Graph g = e->graph_of(L);
-  k_begin<<<1, 1, 0, e->stream>>>(e->d_st, 0, e->opt.width_bits == 16 ? 1 : 0, parity);
+  e->inc_active = false;
+  k_begin<<<1, 1, 0, e->stream>>>(e->d_st, 0, e->opt.width_bits == 16 ? 1 : 0, parity, 0u, e->delta_ratio16);
   k_plan_count<<<(L.nchunks + 255) / 256, 256, 0, e->stream>>>(g, 0);
   k_plan_write<<<1, 1024, 0, e->stream>>>(g);
   if (flag(e, KTG_FLAG_NAIVE_SUPPORT))
@@ -813,6 +1004,16 @@ ktg_status reset(ktg_engine* e) {
   KTG_CUDA(cudaMemcpyAsync(L.deg.p, L.deg_p.p, ((size_t)L.n + 2) * 4, cudaMemcpyDeviceToDevice, s));
   KTG_CUDA(cudaMemsetAsync(L.S0.p, 0, L.slots * 4, s));
   KTG_CUDA(cudaMemsetAsync(L.S1.p, 0, L.slots * 4, s));
+  if (e->reoriented && e->sym_ready) {
+    const size_t nb = (size_t)L.n + 2;
+    KTG_CUDA(cudaMemcpyAsync(e->sym_nbr.p, e->sym_nbr_p.p, e->sym_entries * 4, cudaMemcpyDeviceToDevice, s));
+    KTG_CUDA(cudaMemcpyAsync(e->sym_eid.p, e->sym_eid_p.p, e->sym_entries * 4, cudaMemcpyDeviceToDevice, s));
+    KTG_CUDA(cudaMemcpyAsync(e->sym_deg.p, e->sym_deg_p.p, nb * 4, cudaMemcpyDeviceToDevice, s));
+    KTG_CUDA(cudaMemcpyAsync(e->pos_of.p, e->pos_of_p.p, e->cl.slots * 4, cudaMemcpyDeviceToDevice, s));
+    KTG_CUDA(cudaMemsetAsync(e->dead.p, 0, e->cl.slots, s));
+    KTG_CUDA(cudaMemsetAsync(e->rdirty.p, 0, nb, s));
+    KTG_CUDA(cudaMemsetAsync(e->sdirty.p, 0, nb, s));
+  }
   k_set_live<<<1, 1, 0, s>>>(e->d_st, L.live_pristine);
   KTG_CUDA(cudaGetLastError());
   if (e->reoriented) e->caller_stale = true;

@@ -13,6 +13,7 @@
 // bit-identical to the reference for any schedule.
 #pragma once
 
+#include <cooperative_groups.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -44,6 +45,21 @@ struct DevState {
   unsigned int width16;              // check supports against 65535
   unsigned int pad;
   unsigned long long pairs_needed;   // off-diagonal task capacity (load time)
+  // incremental rounds (working layout, see k_mark / k_delta)
+  unsigned int inc;                  // 1: supports are carried across rounds when cheaper
+  unsigned int mode;                 // this round: 0 = recompute supports, 1 = carried (delta)
+  unsigned int nrq;                  // delta tasks queued by k_mark this round
+  unsigned int delta_ratio16;        // carry when 16 * delta_cost <= ratio16 * keep_cost
+  unsigned int pad2;
+  unsigned long long sum_s;          // sum of S over live edges (k_mark): 3 * triangles
+  unsigned long long delta_cost;     // sum over removed edges of min(du, dv)
+  unsigned long long keep_cost;      // sum over surviving edges of min(du, dv)
+  unsigned long long live_cost;      // keep_cost carried to the next round
+  unsigned int carry;                // this round carries supports (k_decide)
+  unsigned int fpar;                 // frontier queue consumed this round
+  unsigned int nfq[2];               // frontier queue lengths
+  unsigned int nqrow, nqsym;         // rows queued for compaction this round
+  unsigned int nheavy_sym;           // long symmetric rows queued for CTA compaction
 };
 
 struct Graph {
@@ -66,6 +82,31 @@ struct Graph {
   uint32_t scan_ratio;      // SCAN N+(j) when |N+(j)| <= ratio * |tail|
   uint32_t* payload;        // per-slot id compacted along with col (working layout) or null
 };
+
+// Symmetric adjacency of the working layout for incremental rounds: row v
+// lists every live neighbour of v (in-neighbours then out-neighbours, so the
+// row is ascending) with the edge's id (its caller slot, = payload of the
+// oriented entry). Rows are compacted as edges die; symdeg is the live length.
+struct Sym {
+  const unsigned long long* ptr;  // n+2 row offsets
+  uint32_t* nbr;
+  uint32_t* eid;
+  uint32_t* deg;                  // live length of each row
+  uint8_t* dead;                  // per edge id: removed (sticky within a fixpoint)
+  uint8_t* rdirty;                // per vertex: its working row lost an edge this round
+  uint8_t* sdirty;                // per vertex: its symmetric row lost an edge this round
+  uint32_t* qsym;                 // symmetric rows to compact this round
+  uint32_t* qrow;                 // oriented (working) rows to compact this round
+  uint32_t* heavy;                // symmetric rows longer than kHeavyRow (CTA compaction)
+  uint32_t* pos_of;               // per edge id: current working slot of the edge
+  const uint32_t* erow;           // per edge id: its working (oriented) row
+  uint32_t* fq0;                  // frontier queues (edge ids whose carried
+  uint32_t* fq1;                  //   support crossed below k-2), ping-pong
+  uint4* rq;                      // delta tasks {slot, u, v, piece}
+};
+
+constexpr uint32_t kDeadMark = 0x80000000u;  // col mark of an edge removed this round
+constexpr int kDeltaPiece = 256;             // smaller-list elements per delta task
 
 __host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
 
@@ -173,7 +214,7 @@ __global__ void k_chunk_rows(const uint32_t* __restrict__ row_ptr, uint32_t n, u
 
 __global__ void k_plan_count(Graph g, int total) {
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
-  if (q >= g.nchunks) return;
+  if (q >= g.nchunks || g.st->mode) return;
   const uint32_t i = g.chunk_row[q];
   uint32_t cnt = 0;
   if (i >= 1) {
@@ -189,6 +230,7 @@ __global__ void k_plan_count(Graph g, int total) {
 // task counter. 1024 threads.
 __global__ void __launch_bounds__(1024) k_plan_write(Graph g) {
   __shared__ uint32_t warp_sums[32];
+  if (g.st->mode) return;  // supports carried this round
   const uint32_t tid = threadIdx.x;
   const uint32_t Q = g.nchunks;
   const uint32_t per = (Q + blockDim.x - 1) / blockDim.x;
@@ -400,6 +442,7 @@ k_support_chunked(Graph g) {
   constexpr int NW = kSupportThreads / 32;
   constexpr int EPT = kChunk / kSupportThreads;
   constexpr int FPT = kFilterBits / 32 / kSupportThreads;
+  if (g.st->mode) return;  // supports carried this round (incremental mode)
   uint32_t* __restrict__ S = cur_S(g);
   const uint32_t* __restrict__ col = g.col;
   const uint32_t npairs = g.st->npairs;
@@ -886,6 +929,651 @@ k_prune_heavy(Graph g, int fused_reset) {
 }
 
 // ---------------------------------------------------------------------------
+// Incremental rounds (working layout): carry supports across rounds
+// ---------------------------------------------------------------------------
+// A round's supports S_r are exact for the round's graph G_r. Instead of
+// recomputing S_{r+1} from scratch, every triangle of G_r that loses an edge
+// in round r is found once from one of its removed edges and the surviving
+// edges of that triangle lose 1. What is left is exactly the support in
+// G_{r+1} -- the same integers the reference's reset + computeSupports
+// produces (truss.cpp:44-46), so (col, S, removed per round) stay
+// bit-identical; only the work changes. Per round the device picks the
+// cheaper of carrying (delta_cost) and a full pass on the survivors
+// (keep_cost), see k_decide.
+//
+// Round r, mode 0 (after a full support pass): k_mark scans every live edge.
+// Round r, mode 1 (supports carried from r-1): the removals are exactly the
+// edges whose carried support crossed below k-2 during r-1's k_delta, which
+// queued them (frontier); k_mark_frontier handles only those. Rows that lose
+// an edge are queued once (flag bits) for compaction, so a round costs
+// O(removed + their triangles), not O(m).
+
+// Append val to a global queue; one atomic per group of threads that reach
+// the call together (queues are filled from divergent code).
+__device__ __forceinline__ void append_coalesced(uint32_t* cnt, uint32_t* q, uint32_t val) {
+  namespace cg = cooperative_groups;
+  cg::coalesced_group grp = cg::coalesced_threads();
+  uint32_t base = 0;
+  if (grp.thread_rank() == 0) base = atomicAdd(cnt, grp.size());
+  base = grp.shfl(base, 0);
+  q[base + grp.thread_rank()] = val;
+}
+
+// Removal of edge id at working slot p = (u, v): col mark, dead flag, the
+// far endpoint's symmetric row flagged (the caller flags row u), delta
+// tasks. Flags are plain byte stores (every writer stores 1); k_queues turns
+// them into the compaction queues. Returns min(du, dv) (the delta cost).
+__device__ __forceinline__ uint32_t mark_removed(const Graph& g, const Sym& y, uint32_t p, uint32_t u, uint32_t v,
+                                                 uint32_t id, uint32_t* ntask) {
+  g.col[p] = v | kDeadMark;
+  y.dead[id] = 1;
+  y.sdirty[v] = 1;
+  const uint32_t mn = min(y.deg[u], y.deg[v]);
+  *ntask = (mn + kDeltaPiece - 1) / kDeltaPiece;
+  return mn;
+}
+
+// Warp-aggregated append of ntask delta tasks {p, u, v, piece} per lane.
+__device__ __forceinline__ void push_tasks(const Graph& g, const Sym& y, uint32_t ntask, uint32_t p, uint32_t u,
+                                           uint32_t v) {
+  const int lane = threadIdx.x & 31;
+  const unsigned act = __activemask();
+  uint32_t incl = ntask;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const uint32_t t = __shfl_up_sync(act, incl, o);
+    if (lane >= o) incl += t;
+  }
+  const uint32_t total = __shfl_sync(act, incl, 31);
+  if (total == 0) return;
+  uint32_t at = 0;
+  if (lane == 31) at = atomicAdd(&g.st->nrq, total);
+  at = __shfl_sync(act, at, 31) + incl - ntask;
+  for (uint32_t t = 0; t < ntask; ++t) y.rq[at + t] = make_uint4(p, u, v, t);
+}
+
+// Mode 0: warp per row, every live edge; S < k-2 is removed (truss.cpp:31).
+// Totals removed, sum S (3T of G_r), delta cost and keep cost.
+__global__ void __launch_bounds__(kPruneThreads)
+k_mark(Graph g, Sym y) {
+  if (g.st->mode != 0) return;
+  const int lane = threadIdx.x & 31;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  const uint32_t* __restrict__ S = cur_S(g);
+  const uint32_t thr = g.st->threshold;
+  unsigned long long removed = 0, sum_s = 0, dcost = 0, kcost = 0;
+  for (uint32_t u = warp + 1; u <= g.n; u += nwarps) {
+    const uint32_t d = g.deg[u];
+    if (d == 0) continue;
+    const uint32_t base = g.row_ptr[u];
+    for (uint32_t off = 0; off < d; off += 32) {
+      const uint32_t idx = off + lane;
+      uint32_t ntask = 0, v = 0;
+      const uint32_t p = base + idx;
+      bool rm = false;
+      if (idx < d) {
+        v = g.col[p];
+        const uint32_t sv = S[p];
+        sum_s += sv;
+        if (sv < thr) {
+          rm = true;
+          dcost += mark_removed(g, y, p, u, v, g.payload[p], &ntask);
+        } else {
+          kcost += min(y.deg[u], y.deg[v]);
+        }
+      }
+      const unsigned rmask = __ballot_sync(0xffffffffu, rm);
+      if (rmask && lane == 0) {
+        y.rdirty[u] = 1;
+        y.sdirty[u] = 1;
+        removed += __popc(rmask);
+      }
+      push_tasks(g, y, ntask, p, u, v);
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    removed += __shfl_xor_sync(0xffffffffu, removed, o);
+    sum_s += __shfl_xor_sync(0xffffffffu, sum_s, o);
+    dcost += __shfl_xor_sync(0xffffffffu, dcost, o);
+    kcost += __shfl_xor_sync(0xffffffffu, kcost, o);
+  }
+  if (lane == 0) {
+    if (removed) atomicAdd(&g.st->removed, removed);
+    if (sum_s) atomicAdd(&g.st->sum_s, sum_s);
+    if (dcost) atomicAdd(&g.st->delta_cost, dcost);
+    if (kcost) atomicAdd(&g.st->keep_cost, kcost);
+  }
+}
+
+// Mode 1: thread per frontier edge (queued by the previous round's k_delta).
+__global__ void __launch_bounds__(kPruneThreads)
+k_mark_frontier(Graph g, Sym y) {
+  if (g.st->mode != 1) return;
+  const uint32_t par = g.st->fpar;
+  const uint32_t nf = g.st->nfq[par];
+  const uint32_t* __restrict__ fq = par ? y.fq1 : y.fq0;
+  const int lane = threadIdx.x & 31;
+  unsigned long long dcost = 0;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  const uint32_t n_round = (nf + stride - 1) / stride * stride;  // whole warps in every iteration
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_round; i += stride) {
+    uint32_t ntask = 0, p = 0, u = 0, v = 0;
+    if (i < nf) {
+      const uint32_t id = fq[i];
+      p = y.pos_of[id];
+      u = y.erow[id];
+      v = g.col[p];
+      dcost += mark_removed(g, y, p, u, v, id, &ntask);
+      y.rdirty[u] = 1;
+      y.sdirty[u] = 1;
+    }
+    push_tasks(g, y, ntask, p, u, v);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) dcost += __shfl_xor_sync(0xffffffffu, dcost, o);
+  if (lane == 0 && dcost) atomicAdd(&g.st->delta_cost, dcost);
+  if (blockIdx.x == 0 && threadIdx.x == 0) atomicAdd(&g.st->removed, (unsigned long long)nf);
+}
+
+// Thread per vertex: flagged rows -> compaction queues (ballot-aggregated
+// appends, vertex order), flags cleared.
+__global__ void k_queues(Graph g, Sym y) {
+  if (g.st->removed == 0) return;
+  const int lane = threadIdx.x & 31;
+  const uint32_t stride = gridDim.x * blockDim.x;
+  const uint32_t n_round = (g.n + stride - 1) / stride * stride;
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_round; i += stride) {
+    const uint32_t v = i + 1;
+    bool r = false, sy = false;
+    if (v <= g.n) {
+      r = y.rdirty[v];
+      sy = y.sdirty[v];
+      if (r) y.rdirty[v] = 0;
+      if (sy) y.sdirty[v] = 0;
+    }
+    const unsigned mr = __ballot_sync(0xffffffffu, r), ms = __ballot_sync(0xffffffffu, sy);
+    uint32_t br = 0, bs = 0;
+    if (lane == 0) {
+      if (mr) br = atomicAdd(&g.st->nqrow, (uint32_t)__popc(mr));
+      if (ms) bs = atomicAdd(&g.st->nqsym, (uint32_t)__popc(ms));
+    }
+    br = __shfl_sync(0xffffffffu, br, 0);
+    bs = __shfl_sync(0xffffffffu, bs, 0);
+    const unsigned lt = (1u << lane) - 1u;
+    if (r) y.qrow[br + __popc(mr & lt)] = v;
+    if (sy) y.qsym[bs + __popc(ms & lt)] = v;
+  }
+}
+
+// One thread: this round's removal count is final; choose carry vs recompute.
+__global__ void k_decide(DevState* st) {
+  if (st->mode == 1) st->keep_cost = st->live_cost > st->delta_cost ? st->live_cost - st->delta_cost : 0;
+  st->carry = (st->inc && st->removed != 0 &&
+               16ull * st->delta_cost <= (unsigned long long)st->delta_ratio16 * st->keep_cost)
+                  ? 1u
+                  : 0u;
+}
+
+__device__ __forceinline__ uint32_t lb_run(const uint32_t* __restrict__ a, uint32_t n, uint32_t key) {
+  if (n == 0) return 0;
+  const uint32_t* base = a;
+  while (n > 1) {
+    const uint32_t half = n >> 1;
+    base = (__ldg(base + half) < key) ? base + half : base;
+    n -= half;
+  }
+  return (uint32_t)(base - a) + (__ldg(base) < key);
+}
+
+// Surviving edge id at slot p loses one triangle; queue it for the next
+// round when its support crosses below k-2 (exactly once: S only drops by 1).
+__device__ __forceinline__ void drop_support(const Graph& g, const Sym& y, uint32_t* __restrict__ S,
+                                             uint32_t* __restrict__ fq_next, uint32_t* cnt_next, uint32_t thr,
+                                             uint32_t id) {
+  const uint32_t old = atomicSub(&S[y.pos_of[id]], 1u);
+  if (old == thr) append_coalesced(cnt_next, fq_next, id);
+}
+
+// Warp per delta task {slot, u, v, piece}: the removed edge e = (u, v) and a
+// kDeltaPiece window of the shorter of the two symmetric rows; each element w
+// is binary-searched in the longer row. A common neighbour w closes the
+// triangle {e, (u,w), (v,w)} of G_r. It is handled by its removed edge with
+// the smallest id (so once), and each surviving edge of it loses 1.
+__global__ void __launch_bounds__(kPruneThreads)
+k_delta(Graph g, Sym y) {
+  if (!g.st->carry) return;
+  const int lane = threadIdx.x & 31;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  uint32_t* __restrict__ S = cur_S(g);
+  const uint32_t thr = g.st->threshold;
+  const uint32_t par = g.st->fpar ^ 1u;  // next round's frontier
+  uint32_t* __restrict__ fq_next = par ? y.fq1 : y.fq0;
+  uint32_t* cnt_next = &g.st->nfq[par];
+  const uint32_t ntask = g.st->nrq;
+  for (uint32_t t = warp; t < ntask; t += nwarps) {
+    const uint4 q = y.rq[t];
+    const uint32_t e = g.payload[q.x];
+    const uint32_t du = y.deg[q.y], dv = y.deg[q.z];
+    const bool su = du <= dv;
+    const uint32_t la = su ? du : dv, lb = su ? dv : du;
+    const unsigned long long oa = y.ptr[su ? q.y : q.z], ob = y.ptr[su ? q.z : q.y];
+    const uint32_t* __restrict__ A = y.nbr + oa;
+    const uint32_t* __restrict__ B = y.nbr + ob;
+    const uint32_t lo = q.w * kDeltaPiece, hi = min(lo + kDeltaPiece, la);
+    const uint32_t bmin = B[0], bmax = B[lb - 1];
+    for (uint32_t i = lo + lane; i < hi; i += 32) {
+      const uint32_t w = A[i];
+      if (w < bmin || w > bmax) continue;
+      const uint32_t j = lb_run(B, lb, w);
+      if (j < lb && B[j] == w) {
+        const uint32_t ea = y.eid[oa + i], eb = y.eid[ob + j];
+        const bool da = y.dead[ea], db = y.dead[eb];
+        if ((da && ea < e) || (db && eb < e)) continue;
+        if (!da) drop_support(g, y, S, fq_next, cnt_next, thr, ea);
+        if (!db) drop_support(g, y, S, fq_next, cnt_next, thr, eb);
+      }
+    }
+  }
+}
+
+// Oriented rows that lost an edge: stable compaction of (col, id) and, when
+// the round carries supports, S; pos_of follows every moved edge. Warp per
+// queued row up to kHeavyRow (HEAVY = 0), CTA per longer row (HEAVY = 1).
+template <int HEAVY>
+__global__ void __launch_bounds__(kPruneThreads)
+k_inc_rows(Graph g, Sym y) {
+  constexpr int EPT = HEAVY ? 4 : 1;
+  constexpr int NW = kPruneThreads / 32;
+  __shared__ uint32_t red[NW];
+  __shared__ uint32_t tot_s;
+  if (g.st->removed == 0) return;
+  const bool carry = g.st->carry;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint32_t nq = HEAVY ? g.st->nheavy : g.st->nqrow;
+  const uint32_t* __restrict__ queue = HEAVY ? g.heavy_rows : y.qrow;
+  uint32_t* __restrict__ S = cur_S(g);
+  uint32_t* __restrict__ col = g.col;
+  uint32_t* __restrict__ pay = g.payload;
+  const uint32_t first = HEAVY ? blockIdx.x : (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t step = HEAVY ? gridDim.x : (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t h = first; h < nq; h += step) {
+    const uint32_t u = queue[h];
+    const uint32_t d = g.deg[u];
+    if (!HEAVY && d > (uint32_t)kHeavyRow) {  // long row: CTA kernel
+      if (lane == 0) g.heavy_rows[atomicAdd(&g.st->nheavy, 1u)] = u;
+      continue;
+    }
+    const uint32_t base = g.row_ptr[u];
+    uint32_t write = 0;
+    constexpr uint32_t TILE = HEAVY ? EPT * kPruneThreads : 32;
+    for (uint32_t off = 0; off < d; off += TILE) {
+      uint32_t c[EPT], sv[EPT], pv[EPT];
+      bool keep[EPT];
+      uint32_t cnt = 0;
+#pragma unroll
+      for (int k = 0; k < EPT; ++k) {
+        const uint32_t idx = off + (HEAVY ? threadIdx.x * EPT + k : lane);
+        const bool live = idx < d;
+        c[k] = live ? col[base + idx] : 0u;
+        sv[k] = (live && carry) ? S[base + idx] : 0u;
+        pv[k] = live ? pay[base + idx] : 0u;
+        keep[k] = live && !(c[k] & kDeadMark);
+        cnt += keep[k];
+      }
+      uint32_t x = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += t;
+      }
+      uint32_t pos, total;
+      if (HEAVY) {
+        if (lane == 31) red[wid] = x;
+        __syncthreads();  // also: every thread has read its tile before writes
+        if (wid == 0) {
+          uint32_t w = lane < NW ? red[lane] : 0;
+#pragma unroll
+          for (int o = 1; o < NW; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += t;
+          }
+          if (lane < NW) red[lane] = w;
+          if (lane == NW - 1) tot_s = w;
+        }
+        __syncthreads();
+        pos = write + x - cnt + (wid ? red[wid - 1] : 0);
+        total = tot_s;
+      } else {
+        __syncwarp();  // every lane's loads precede any lane's in-place store
+        pos = write + x - cnt;
+        total = __shfl_sync(0xffffffffu, x, 31);
+      }
+#pragma unroll
+      for (int k = 0; k < EPT; ++k) {
+        const uint32_t idx = off + (HEAVY ? threadIdx.x * EPT + k : lane);
+        if (keep[k]) {
+          col[base + pos] = c[k];
+          if (carry) S[base + pos] = sv[k];
+          pay[base + pos] = pv[k];
+          if (pos != idx) y.pos_of[pv[k]] = base + pos;
+          ++pos;
+        }
+      }
+      write += total;
+      if (HEAVY) __syncthreads();
+    }
+    for (uint32_t x = write + (HEAVY ? threadIdx.x : lane); x < d; x += (HEAVY ? blockDim.x : 32)) {
+      col[base + x] = 0;
+      if (carry) S[base + x] = 0;
+    }
+    if (HEAVY ? threadIdx.x == 0 : lane == 0) g.deg[u] = write;
+    if (HEAVY) __syncthreads();
+  }
+}
+
+// Symmetric rows that lost an edge drop their dead entries (stable).
+template <int HEAVY>
+__global__ void __launch_bounds__(kPruneThreads)
+k_inc_sym(Graph g, Sym y) {
+  constexpr int EPT = HEAVY ? 4 : 1;
+  constexpr int NW = kPruneThreads / 32;
+  __shared__ uint32_t red[NW];
+  __shared__ uint32_t tot_s;
+  if (g.st->removed == 0) return;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint32_t nq = HEAVY ? g.st->nheavy_sym : g.st->nqsym;
+  const uint32_t* __restrict__ queue = HEAVY ? y.heavy : y.qsym;
+  const uint32_t first = HEAVY ? blockIdx.x : (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t step = HEAVY ? gridDim.x : (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t h = first; h < nq; h += step) {
+    const uint32_t v = queue[h];
+    const uint32_t d = y.deg[v];
+    if (!HEAVY && d > (uint32_t)kHeavyRow) {  // long row: CTA kernel
+      if (lane == 0) y.heavy[atomicAdd(&g.st->nheavy_sym, 1u)] = v;
+      continue;
+    }
+    const unsigned long long base = y.ptr[v];
+    uint32_t write = 0;
+    constexpr uint32_t TILE = HEAVY ? EPT * kPruneThreads : 32;
+    for (uint32_t off = 0; off < d; off += TILE) {
+      uint32_t w[EPT], ev[EPT];
+      bool keep[EPT];
+      uint32_t cnt = 0;
+#pragma unroll
+      for (int k = 0; k < EPT; ++k) {
+        const uint32_t idx = off + (HEAVY ? threadIdx.x * EPT + k : lane);
+        const bool live = idx < d;
+        w[k] = live ? y.nbr[base + idx] : 0u;
+        ev[k] = live ? y.eid[base + idx] : 0u;
+        keep[k] = live && !y.dead[ev[k]];
+        cnt += keep[k];
+      }
+      uint32_t x = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += t;
+      }
+      uint32_t pos, total;
+      if (HEAVY) {
+        if (lane == 31) red[wid] = x;
+        __syncthreads();
+        if (wid == 0) {
+          uint32_t s = lane < NW ? red[lane] : 0;
+#pragma unroll
+          for (int o = 1; o < NW; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, s, o);
+            if (lane >= o) s += t;
+          }
+          if (lane < NW) red[lane] = s;
+          if (lane == NW - 1) tot_s = s;
+        }
+        __syncthreads();
+        pos = write + x - cnt + (wid ? red[wid - 1] : 0);
+        total = tot_s;
+      } else {
+        __syncwarp();
+        pos = write + x - cnt;
+        total = __shfl_sync(0xffffffffu, x, 31);
+      }
+#pragma unroll
+      for (int k = 0; k < EPT; ++k)
+        if (keep[k]) {
+          y.nbr[base + pos] = w[k];
+          y.eid[base + pos] = ev[k];
+          ++pos;
+        }
+      write += total;
+      if (HEAVY) __syncthreads();
+    }
+    if (HEAVY ? threadIdx.x == 0 : lane == 0) y.deg[v] = write;
+    if (HEAVY) __syncthreads();
+  }
+}
+
+// Publish after a carried run, one pass per caller row: caller slot s
+// survives iff its edge is not dead; survivors are compacted stably from the
+// pristine row (the composition of every round's prune, truss.cpp:26-35) and
+// take their support from the working slot pos_of[s]. Warp per row up to
+// kHeavyRow (HEAVY = 0, longer rows queued), CTA per longer row (HEAVY = 1).
+template <int HEAVY>
+__global__ void __launch_bounds__(kPruneThreads)
+k_publish_inc(Graph c, const uint32_t* __restrict__ col_p, const uint32_t* __restrict__ deg_p,
+              const uint8_t* __restrict__ dead, const uint32_t* __restrict__ pos_of,
+              const uint32_t* __restrict__ Sw) {
+  constexpr int EPT = HEAVY ? 4 : 1;
+  constexpr int NW = kPruneThreads / 32;
+  __shared__ uint32_t red[NW];
+  __shared__ uint32_t tot_s;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const uint32_t nq = HEAVY ? c.st->nheavy : c.n;
+  const uint32_t first = HEAVY ? blockIdx.x : (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t step = HEAVY ? gridDim.x : (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t h = first; h < nq; h += step) {
+    const uint32_t r = HEAVY ? c.heavy_rows[h] : h + 1;
+    const uint32_t d = deg_p[r];
+    if (d == 0) continue;
+    if (!HEAVY && d > (uint32_t)kHeavyRow) {
+      if (lane == 0) c.heavy_rows[atomicAdd(&c.st->nheavy, 1u)] = r;
+      continue;
+    }
+    const uint32_t base = c.row_ptr[r];
+    uint32_t write = 0;
+    constexpr uint32_t TILE = HEAVY ? EPT * kPruneThreads : 32;
+    for (uint32_t off = 0; off < d; off += TILE) {
+      uint32_t cv[EPT], sv[EPT];
+      bool keep[EPT];
+      uint32_t cnt = 0;
+#pragma unroll
+      for (int k = 0; k < EPT; ++k) {
+        const uint32_t idx = off + (HEAVY ? threadIdx.x * EPT + k : lane);
+        keep[k] = idx < d && !dead[base + idx];
+        cv[k] = keep[k] ? col_p[base + idx] : 0u;
+        sv[k] = keep[k] ? Sw[pos_of[base + idx]] : 0u;
+        cnt += keep[k];
+      }
+      uint32_t x = cnt;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += t;
+      }
+      uint32_t pos, total;
+      if (HEAVY) {
+        if (lane == 31) red[wid] = x;
+        __syncthreads();
+        if (wid == 0) {
+          uint32_t w = lane < NW ? red[lane] : 0;
+#pragma unroll
+          for (int o = 1; o < NW; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += t;
+          }
+          if (lane < NW) red[lane] = w;
+          if (lane == NW - 1) tot_s = w;
+        }
+        __syncthreads();
+        pos = write + x - cnt + (wid ? red[wid - 1] : 0);
+        total = tot_s;
+      } else {
+        pos = write + x - cnt;
+        total = __shfl_sync(0xffffffffu, x, 31);
+      }
+#pragma unroll
+      for (int k = 0; k < EPT; ++k)
+        if (keep[k]) {
+          c.col[base + pos] = cv[k];
+          c.S0[base + pos] = sv[k];
+          ++pos;
+        }
+      write += total;
+      if (HEAVY) __syncthreads();
+    }
+    for (uint32_t x = write + (HEAVY ? threadIdx.x : lane); x < d; x += (HEAVY ? blockDim.x : 32)) {
+      c.col[base + x] = 0;
+      c.S0[base + x] = 0;
+    }
+    if (HEAVY ? threadIdx.x == 0 : lane == 0) c.deg[r] = write;
+    if (HEAVY) __syncthreads();
+  }
+}
+
+// A recompute round follows: zero S (the next full pass accumulates into it).
+__global__ void k_inc_zero(Graph g) {
+  if (g.st->removed == 0 || g.st->carry) return;
+  uint4* S4 = reinterpret_cast<uint4*>(cur_S(g));
+  const uint64_t n4 = (g.slots + 3) / 4;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n4; i += (uint64_t)gridDim.x * blockDim.x)
+    S4[i] = make_uint4(0, 0, 0, 0);
+}
+
+// End of an incremental round: removal history, live count, the next round's
+// mode and frontier, the while condition. S stays in one buffer.
+__global__ void k_control_inc(DevState* st, unsigned long long* hist, cudaGraphConditionalHandle handle,
+                              int use_cond) {
+  const unsigned long long removed = st->removed;
+  const uint32_t it = st->iter;
+  if (it < (uint32_t)kHistCap) hist[it] = removed;
+  st->iter = it + 1;
+  st->live -= removed;
+  if (st->mode == 0) st->last_triangles = st->sum_s / 3;
+  st->live_cost = st->keep_cost;
+  st->mode = st->carry;
+  st->nfq[st->fpar] = 0;
+  st->fpar ^= 1u;
+  st->carry = 0;
+  st->triangles = 0;
+  st->sum_s = 0;
+  st->delta_cost = 0;
+  st->keep_cost = 0;
+  st->nrq = 0;
+  st->nqrow = 0;
+  st->nqsym = 0;
+  st->nheavy_sym = 0;
+  st->removed = 0;
+  st->task_next = 0;
+  st->nheavy = 0;
+  const bool cont = removed != 0 && st->error == 0;
+  if (use_cond) cudaGraphSetConditional(handle, cont ? 1u : 0u);
+}
+
+// T of the converged graph (sum of its supports / 3) after a carried run.
+__global__ void k_inc_triangles(Graph g) {
+  const uint32_t* __restrict__ S = cur_S(g);
+  unsigned long long s = 0;
+  const uint4* S4 = reinterpret_cast<const uint4*>(S);
+  const uint64_t n4 = (g.slots + 3) / 4;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n4; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint4 q = S4[i];
+    s += (unsigned long long)q.x + q.y + q.z + q.w;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0 && s) atomicAdd(&g.st->sum_s, s);
+}
+
+__global__ void k_inc_triangles_done(DevState* st) {
+  st->last_triangles = st->sum_s / 3;
+  st->sum_s = 0;
+}
+
+// Symmetric adjacency build (load time). In-neighbour keys (v << B | u) for
+// every live working edge u -> v, with the edge id as value; sorted, they
+// give each row's in-part in ascending order.
+__global__ void k_sym_in_keys(Graph w, uint32_t B, unsigned long long* __restrict__ keys,
+                              uint32_t* __restrict__ vals, const unsigned long long* __restrict__ offs) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t u = warp + 1; u <= w.n; u += nwarps) {
+    const uint32_t d = w.deg[u], base = w.row_ptr[u];
+    const unsigned long long o = offs[u];
+    for (uint32_t x = lane; x < d; x += 32) {
+      keys[o + x] = ((unsigned long long)w.col[base + x] << B) | u;
+      vals[o + x] = w.payload[base + x];
+    }
+  }
+}
+
+// Row v of the symmetric adjacency = sorted in-part (indices [inoff[v],
+// inoff[v]+din[v]) of the sorted keys) followed by the out-part (working row v).
+__global__ void k_sym_fill(Graph w, uint32_t B, const unsigned long long* __restrict__ keys,
+                           const uint32_t* __restrict__ vals, const unsigned long long* __restrict__ inoff,
+                           const uint32_t* __restrict__ din, Sym y) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  const unsigned long long mask = (1ull << B) - 1;
+  for (uint32_t v = warp + 1; v <= w.n; v += nwarps) {
+    const unsigned long long dst = y.ptr[v], io = inoff[v];
+    const uint32_t di = din[v], d = w.deg[v], base = w.row_ptr[v];
+    for (uint32_t x = lane; x < di; x += 32) {
+      y.nbr[dst + x] = (uint32_t)(keys[io + x] & mask);
+      y.eid[dst + x] = vals[io + x];
+    }
+    for (uint32_t x = lane; x < d; x += 32) {
+      y.nbr[dst + di + x] = w.col[base + x];
+      y.eid[dst + di + x] = w.payload[base + x];
+    }
+    if (lane == 0) y.deg[v] = di + d;
+  }
+}
+
+// pos_of for the pristine working layout, and the delta queue capacity: one
+// task per kDeltaPiece elements of min(du, dv) over every edge -- degrees only
+// shrink, so no round can queue more.
+__global__ void k_sym_pos(Graph w, Sym y, unsigned long long* __restrict__ cap) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  unsigned long long c = 0;
+  for (uint32_t u = warp + 1; u <= w.n; u += nwarps) {
+    const uint32_t d = w.deg[u], base = w.row_ptr[u], du = y.deg[u];
+    for (uint32_t x = lane; x < d; x += 32) {
+      y.pos_of[w.payload[base + x]] = base + x;
+      const_cast<uint32_t*>(y.erow)[w.payload[base + x]] = u;
+      const uint32_t mn = min(du, y.deg[w.col[base + x]]);
+      c += (mn + kDeltaPiece - 1) / kDeltaPiece;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if (lane == 0 && c) atomicAdd(cap, c);
+}
+
+__global__ void k_add_u64(const unsigned long long* __restrict__ a, const unsigned long long* __restrict__ b,
+                          uint32_t n, unsigned long long* __restrict__ c) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) c[i] = a[i] + b[i];
+}
+
+__global__ void k_u32_to_u64(const uint32_t* __restrict__ a, uint32_t n, unsigned long long* __restrict__ b) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) b[i] = a[i];
+}
+
+// ---------------------------------------------------------------------------
 // canonicalize + build_csr on the device
 // ---------------------------------------------------------------------------
 // Same result as edge_list.cpp:62-103 + csr.cpp:10-32: self-loops dropped,
@@ -1022,7 +1710,21 @@ __global__ void k_scatter_live(Graph w, const uint32_t* __restrict__ col_pristin
 // ---------------------------------------------------------------------------
 // Loop control
 // ---------------------------------------------------------------------------
-__global__ void k_begin(DevState* st, uint32_t threshold, uint32_t width16, int parity) {
+__global__ void k_begin(DevState* st, uint32_t threshold, uint32_t width16, int parity, uint32_t inc,
+                        uint32_t delta_ratio16) {
+  st->inc = inc;
+  st->mode = 0;
+  st->nrq = 0;
+  st->carry = 0;
+  st->fpar = 0;
+  st->nfq[0] = st->nfq[1] = 0;
+  st->nqrow = st->nqsym = 0;
+  st->nheavy_sym = 0;
+  st->live_cost = 0;
+  st->delta_ratio16 = delta_ratio16;
+  st->sum_s = 0;
+  st->delta_cost = 0;
+  st->keep_cost = 0;
   st->removed = 0;
   st->triangles = 0;
   st->last_triangles = 0;

@@ -88,6 +88,7 @@ class TrussOptions:
     host_loop: bool = False
     naive_support: bool = False
     label_order: bool = False   # run on the caller's CSR, not the degree-ordered copy
+    recompute: bool = False     # full support pass every round (no carried supports)
     device: int = -1
 
 
@@ -156,6 +157,7 @@ FLAG_NAIVE_SUPPORT = 2
 FLAG_COLLECT_WORK = 4
 FLAG_TIME_SUPPORT = 8
 FLAG_LABEL_ORDER = 16
+FLAG_RECOMPUTE = 32
 
 _configured = False
 
@@ -250,6 +252,8 @@ def _options(o: Optional[TrussOptions], keep=None) -> _Options:
         flags |= FLAG_NAIVE_SUPPORT
     if o.label_order:
         flags |= FLAG_LABEL_ORDER
+    if o.recompute:
+        flags |= FLAG_RECOMPUTE
     c.flags = flags
     if o.observer is not None and keep is not None:
         obs = o.observer

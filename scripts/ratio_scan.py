@@ -1,0 +1,25 @@
+"""Fixpoint time per K under different carry/recompute cost ratios
+(KTG_DELTA_RATIO), to calibrate delta_round's cost model."""
+import os, sys, time
+sys.path.insert(0, ".")
+import paper_2009_07929_b200 as kt
+g = kt.rmat(int(os.environ.get("SCALE", "20")))
+ks = [3, 5, 10, 20, 30, 45, 60, 80, 100, 110, 120, 135, 150, 165, 180, 200, 215, 230, 260, 304]
+ratios = sys.argv[1:] or ["0", "0.05", "0.1", "0.2", "0.5", "1", "1e9"]
+res = {}
+for r in ratios:
+    os.environ["KTG_DELTA_RATIO"] = r
+    eng = kt.Engine(g)
+    row = []
+    for k in ks:
+        best = 1e9
+        for _ in range(2):
+            eng.reset(); eng.run(k)
+            best = min(best, eng.info()["device_ms"])
+        row.append(best)
+    res[r] = row
+    eng.close()
+print("K      " + " ".join(f"{r:>8s}" for r in ratios))
+for i, k in enumerate(ks):
+    print(f"{k:5d}  " + " ".join(f"{res[r][i]:8.2f}" for r in ratios))
+print("sum    " + " ".join(f"{sum(res[r]):8.1f}" for r in ratios))

@@ -27,10 +27,34 @@ def s14():
     return kt.rmat(14)
 
 
-@pytest.mark.parametrize("label", [False, True])
-def test_s14_every_k_byte_exact(s14, port, label):
+# label: caller layout, full pass per round. recompute: working layout, full
+# pass per round. inc: carried supports where cheaper (default). delta /
+# delta_host: carried supports every round after the first (forced by the
+# cost ratio), device loop / host loop.
+MODES = {
+    "label": (dict(label_order=True), None, {}),
+    "recompute": (dict(recompute=True), None, {}),
+    "inc": ({}, None, {}),
+    "delta": ({}, "1e9", {}),
+    "delta_host": (dict(host_loop=True), "1e9", dict(time_support=True)),
+}
+
+
+def mode_engine(g, mode, monkeypatch):
+    opts, ratio, extra = MODES[mode]
+    if ratio is not None:
+        monkeypatch.setenv("KTG_DELTA_RATIO", ratio)
+    else:
+        monkeypatch.delenv("KTG_DELTA_RATIO", raising=False)
+    eng = kt.Engine(g, kt.TrussOptions(**opts), **extra)
+    monkeypatch.delenv("KTG_DELTA_RATIO", raising=False)
+    return eng
+
+
+@pytest.mark.parametrize("mode", list(MODES))
+def test_s14_every_k_byte_exact(s14, port, mode, monkeypatch):
     ent = golden("rmat.json")["s14_known"]
-    eng = kt.Engine(s14, kt.TrussOptions(label_order=label))
+    eng = mode_engine(s14, mode, monkeypatch)
     for k in range(3, ent["kmax"] + 2):
         eng.reset()
         hist = eng.run(k)
@@ -38,6 +62,7 @@ def test_s14_every_k_byte_exact(s14, port, label):
         col_e, S_e, hist_e = port.run_fixpoint(s14, k, threads=8)
         assert hist == hist_e, k
         assert np.array_equal(col, col_e) and np.array_equal(S, S_e), k
+        assert eng.info()["triangles"] * 3 == int(S_e.sum(dtype=np.uint64)), k
         if k == 3:
             assert eng.info()["live_edges"] == ent["k3_survivors"]
         if k == ent["kmax"]:
@@ -129,9 +154,9 @@ def test_s20_known_answers_and_properties(s20):
     assert eng.info()["live_edges"] == ent["kmax_survivors"]
 
 
-@pytest.mark.parametrize("k,label", [(3, False), (304, False), (3, True)])
-def test_s20_byte_exact(s20, port, k, label):
-    eng = kt.Engine(s20, kt.TrussOptions(label_order=label))
+@pytest.mark.parametrize("k,mode", [(3, "inc"), (304, "inc"), (3, "label"), (30, "delta"), (120, "recompute")])
+def test_s20_byte_exact(s20, port, k, mode, monkeypatch):
+    eng = mode_engine(s20, mode, monkeypatch)
     eng.reset()
     hist = eng.run(k)
     col, S = eng.read()
