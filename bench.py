@@ -277,13 +277,17 @@ def main():
             eng.run(k, sync=False)
 
     launches_per_k = {}
+    rounds_per_k = {}
     live_per_k = {}
     # one synchronous pass: iterations per K (for the launch count) + checks
     for k in mine:
         eng.reset()
         h = eng.run(k)
-        # k_set_live + k_begin + 6 per round + 5 publish (degree-ordered layout)
-        launches_per_k[k] = 2 + 6 * len(h) + 5
+        # k_set_live + k_begin + 14 per round (plan x2, support, mark x2, decide,
+        # queues, delta, rows x2, sym x2, zero, control; the ones a round does
+        # not need exit at once) + 2 triangle total + 4 publish
+        launches_per_k[k] = 2 + 14 * len(h) + 2 + 4
+        rounds_per_k[k] = len(h)
         live_per_k[k] = eng.info()["live_edges"]
 
     for _ in range(args.warmup):
@@ -328,7 +332,7 @@ def main():
         e1.synchronize()
         incr_ms = e0.elapsed_time(e1)
         incr = {"ms": incr_ms, "value": total_k * m / (incr_ms / 1e3), "unit": "edges/s", "rounds": iters,
-                "pristine_rounds": sum((launches_per_k[k] - 7) // 6 for k in ks),
+                "pristine_rounds": sum(rounds_per_k.values()),
                 "survivors_equal_pristine": bool(same),
                 "note": "each K from the (K-1)-truss; not the headline (value is pristine per K)"}
 
@@ -366,8 +370,10 @@ def main():
         except Exception:
             peak, peak_src = 6650.0, "fallback"
         sample_k = sorted(set([ks[0]] + ks[len(ks) // 4::max(1, len(ks) // 4)] + [ks[-1]]))
-        ew = kt.Engine(g, collect_work=True)
-        et = kt.Engine(g, time_support=True)
+        # full support passes every round (recompute mode): each launch is a
+        # whole-graph pass whose algorithmic bytes are the §8(d) formula
+        ew = kt.Engine(g, kt.TrussOptions(recompute=True), collect_work=True)
+        et = kt.Engine(g, kt.TrussOptions(recompute=True), time_support=True)
         tot_b = tot_ms = 0.0
         n_launch = 0
         fix_b = 0.0
@@ -379,6 +385,8 @@ def main():
             et.run(k)
             tw = et.round_work()
             for w, t in zip(work, tw):
+                if not t["full_pass"]:  # supports carried: the launch exits at once
+                    continue
                 tot_b += support_bytes(w, n, slots)
                 tot_ms += t["support_ms"]
                 n_launch += 1
@@ -492,7 +500,9 @@ def run_fixpoint_mode(args):
         kd.engine_join(eng)
     eng.reset()
     hist = eng.run(k)
-    launches = 2 + 6 * len(hist) + 5
+    # carried-support rounds on one rank (14 launches per round + 2 + 4);
+    # the partitioned multi-rank loop recomputes (6 per round + 5 publish)
+    launches = (2 + 14 * len(hist) + 2 + 4) if world == 1 else (2 + 6 * len(hist) + 5)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     for _ in range(args.warmup):
         eng.reset()
@@ -538,17 +548,20 @@ def run_fixpoint_mode(args):
             peak, src = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"]), "measured"
         except Exception:
             peak, src = 6650.0, "fallback"
-        ew = kt.Engine(g, collect_work=True)
-        et = kt.Engine(g, time_support=True)
+        # full support passes every round (recompute mode): each launch is a
+        # whole-graph pass whose algorithmic bytes are the §8(d) formula
+        ew = kt.Engine(g, kt.TrussOptions(recompute=True), collect_work=True)
+        et = kt.Engine(g, kt.TrussOptions(recompute=True), time_support=True)
         ew.reset(); ew.run(k); w = ew.round_work()
         et.reset(); et.run(k); tw = et.round_work()
         ew.close(); et.close()
-        tb = sum(support_bytes(x, n, slots) for x in w)
-        tm = sum(x["support_ms"] for x in tw)
+        full = [(x, t) for x, t in zip(w, tw) if t["full_pass"]]  # carried rounds skip the kernel
+        tb = sum(support_bytes(x, n, slots) for x, _ in full)
+        tm = sum(t["support_ms"] for _, t in full)
         achieved = tb / (tm / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": None, "peak_source": src,
-                "kernel": "k_support_chunked", "launches_measured": len(tw)}
+                "kernel": "k_support_chunked", "launches_measured": len(full)}
         if world == 1 and not args.no_cpu_baseline:
             v, desc = cpu_port_sample(g, k, args.cpu_budget_s, 1)
             cpu = {"value": v, "unit": "edges/s", "cores": 1, "kind": "port", "sample": desc}

@@ -76,13 +76,18 @@ enum {
   KTG_FLAG_LABEL_ORDER = 1u << 4,   /* run the fixpoint on the caller's (label-
                                        ordered) CSR instead of the internal
                                        degree-ordered working copy */
-  KTG_FLAG_RECOMPUTE = 1u << 5      /* recompute every round's supports from
+  KTG_FLAG_RECOMPUTE = 1u << 5,     /* recompute every round's supports from
                                        scratch (reset + computeSupports,
                                        truss.cpp:44-46) instead of carrying
                                        them: the default working-layout run
                                        decrements the supports of triangles
                                        that lose an edge whenever that is
                                        cheaper (same S, same rounds) */
+  KTG_FLAG_NO_DEGREE_BOUND = 1u << 6 /* carried runs from the pristine graph
+                                       skip round-0 pivots that cannot reach a
+                                       possible survivor (support <= min
+                                       degree - 1); this flag turns that off
+                                       (results are identical either way) */
 };
 
 typedef struct {
@@ -183,6 +188,9 @@ typedef struct {
   uint64_t triangles;   /* triangles found in the round              */
   uint64_t removed;     /* edges pruned by the round                 */
   double support_ms;    /* support kernel time (KTG_FLAG_TIME_SUPPORT) */
+  uint32_t full_pass;   /* 1: the round ran a full support pass; 0: its
+                           supports were carried from the previous round */
+  uint32_t pad;
 } ktg_round_work;
 
 ktg_status ktg_engine_create(const ktg_options* opt, ktg_engine** out);

@@ -173,6 +173,7 @@ struct ktg_engine {
   uint64_t sym_entries = 0, rq_cap = 0;
   bool sym_ready = false;
   bool inc_active = false;    // the current fixpoint carries supports
+  bool pristine = false;      // the working layout holds the pristine graph (after load / reset)
   uint32_t delta_ratio16 = 1;  // carry when delta_cost <= keep_cost / 16 (s20 sweep calibration, scripts/ratio_scan.py)
 
   unsigned long long* d_workL = nullptr;
@@ -527,6 +528,7 @@ ktg_status build_sym(ktg_engine* e) {
   e->rq_cap = cap;
   KTG_TRY(e->rq.ensure(cap));
   e->sym_ready = true;
+  e->pristine = true;
   return KTG_OK;
 }
 
@@ -810,6 +812,9 @@ ktg_status begin_run(ktg_engine* e, uint32_t k, int parity) {
   }
   k_begin<<<1, 1, 0, e->stream>>>(e->d_st, k >= 2 ? k - 2 : 0, e->opt.width_bits == 16 ? 1 : 0, parity,
                                   e->inc_active ? 1u : 0u, e->delta_ratio16);
+  if (e->inc_active && e->pristine && !flag(e, KTG_FLAG_NO_DEGREE_BOUND))
+    k_heavy_rank<<<1, 1, 0, e->stream>>>(e->d_st, e->sym_deg_p.p, e->wl.n);
+  e->pristine = false;
   KTG_CUDA(cudaGetLastError());
   return KTG_OK;
 }
@@ -873,6 +878,7 @@ ktg_status run_loop(ktg_engine* e, bool want_sync) {
     uint32_t* Sc = e->h_st->parity ? L.S1.p : L.S0.p;
     if (!e->inc_active) KTG_CUDA(cudaMemsetAsync(Sc, 0, L.slots * 4, e->stream));
     ktg_round_work w{};
+    w.full_pass = e->h_st->mode == 0 ? 1u : 0u;  // state read after the previous round
     if (flag(e, KTG_FLAG_COLLECT_WORK)) KTG_TRY(collect_work(e, &w));
     KTG_TRY(enqueue_round(e, false, 0, timing ? e->evs0 : nullptr, timing ? e->evs1 : nullptr));
     KTG_TRY(read_state(e));
@@ -1017,6 +1023,7 @@ ktg_status reset(ktg_engine* e) {
   k_set_live<<<1, 1, 0, s>>>(e->d_st, L.live_pristine);
   KTG_CUDA(cudaGetLastError());
   if (e->reoriented) e->caller_stale = true;
+  e->pristine = true;
   return KTG_OK;
 }
 

@@ -60,6 +60,7 @@ struct DevState {
   unsigned int nfq[2];               // frontier queue lengths
   unsigned int nqrow, nqsym;         // rows queued for compaction this round
   unsigned int nheavy_sym;           // long symmetric rows queued for CTA compaction
+  unsigned int h0;                   // round 0 from pristine: first rank of degree >= k-1 (0: off)
 };
 
 struct Graph {
@@ -448,6 +449,7 @@ k_support_chunked(Graph g) {
   const uint32_t npairs = g.st->npairs;
   const uint32_t ntasks = npairs + g.nchunks;
   const uint32_t ratio = g.scan_ratio;
+  const uint32_t h0 = g.st->h0;  // pivots (i, j) with j < h0 cannot matter (see k_heavy_rank)
   const unsigned lt_mask = (1u << lane) - 1u;
   unsigned long long tri_local = 0;
 
@@ -549,7 +551,7 @@ k_support_chunked(Graph g) {
       if (x >= pstart && x < plen) {
         const uint32_t j = diag ? s.A[x] : col[p0 + x];
         const uint32_t tb_ = diag ? x + 1 : 0;
-        if (j != 0 && tb_ < alen) {
+        if (j >= h0 && j != 0 && tb_ < alen) {
           const uint32_t te_ = s.nz[tb_];
           if (te_ > tb_) {
             const uint32_t dj = g.deg[j];
@@ -1002,6 +1004,7 @@ k_mark(Graph g, Sym y) {
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
   const uint32_t* __restrict__ S = cur_S(g);
   const uint32_t thr = g.st->threshold;
+  const uint32_t h0 = g.st->h0;
   unsigned long long removed = 0, sum_s = 0, dcost = 0, kcost = 0;
   for (uint32_t u = warp + 1; u <= g.n; u += nwarps) {
     const uint32_t d = g.deg[u];
@@ -1016,7 +1019,7 @@ k_mark(Graph g, Sym y) {
         v = g.col[p];
         const uint32_t sv = S[p];
         sum_s += sv;
-        if (sv < thr) {
+        if (sv < thr || u < h0) {
           rm = true;
           dcost += mark_removed(g, y, p, u, v, g.payload[p], &ntask);
         } else {
@@ -1105,6 +1108,24 @@ __global__ void k_queues(Graph g, Sym y) {
     if (r) y.qrow[br + __popc(mr & lt)] = v;
     if (sy) y.qsym[bs + __popc(ms & lt)] = v;
   }
+}
+
+// Round 0 of a fixpoint from the pristine graph (ranks ascend by undirected
+// degree, so symdeg_p is non-decreasing in rank): an edge (u, v), u < v,
+// has S <= min(du, dv) - 1 = du - 1, so every edge of a row u with
+// du < k-1 goes in round 0 whatever its count (truss.cpp:31), and a triangle
+// matters for a possible survivor only through pivots (i, j) with j heavy
+// (dj >= k-1; then the tail and N+(j) are heavy too). h0 = first heavy
+// rank: k_support_chunked skips pivots j < h0, k_mark removes rows u < h0.
+// The round's removals (count and set) and every later round are unchanged.
+__global__ void k_heavy_rank(DevState* st, const uint32_t* __restrict__ symdeg_p, uint32_t n) {
+  const uint32_t need = st->threshold + 1;  // k - 1
+  uint32_t lo = 1, hi = n + 1;              // first rank r in [1, n] with symdeg_p[r] >= need
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (symdeg_p[mid] < need) lo = mid + 1; else hi = mid;
+  }
+  st->h0 = lo;
 }
 
 // One thread: this round's removal count is final; choose carry vs recompute.
@@ -1462,6 +1483,7 @@ __global__ void k_control_inc(DevState* st, unsigned long long* hist, cudaGraphC
   if (st->mode == 0) st->last_triangles = st->sum_s / 3;
   st->live_cost = st->keep_cost;
   st->mode = st->carry;
+  st->h0 = 0;  // round 0 only
   st->nfq[st->fpar] = 0;
   st->fpar ^= 1u;
   st->carry = 0;
@@ -1720,6 +1742,7 @@ __global__ void k_begin(DevState* st, uint32_t threshold, uint32_t width16, int 
   st->nfq[0] = st->nfq[1] = 0;
   st->nqrow = st->nqsym = 0;
   st->nheavy_sym = 0;
+  st->h0 = 0;
   st->live_cost = 0;
   st->delta_ratio16 = delta_ratio16;
   st->sum_s = 0;

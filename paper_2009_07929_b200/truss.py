@@ -89,6 +89,7 @@ class TrussOptions:
     naive_support: bool = False
     label_order: bool = False   # run on the caller's CSR, not the degree-ordered copy
     recompute: bool = False     # full support pass every round (no carried supports)
+    no_degree_bound: bool = False  # round 0 counts every pivot (no min-degree skip)
     device: int = -1
 
 
@@ -149,7 +150,7 @@ class _RunInfo(ctypes.Structure):
 
 class _RoundWork(ctypes.Structure):
     _fields_ = [("live_edges", _u64), ("L", _u64), ("triangles", _u64), ("removed", _u64),
-                ("support_ms", ctypes.c_double)]
+                ("support_ms", ctypes.c_double), ("full_pass", ctypes.c_uint32), ("pad", ctypes.c_uint32)]
 
 
 FLAG_HOST_LOOP = 1
@@ -158,6 +159,7 @@ FLAG_COLLECT_WORK = 4
 FLAG_TIME_SUPPORT = 8
 FLAG_LABEL_ORDER = 16
 FLAG_RECOMPUTE = 32
+FLAG_NO_DEGREE_BOUND = 64
 
 _configured = False
 
@@ -254,6 +256,8 @@ def _options(o: Optional[TrussOptions], keep=None) -> _Options:
         flags |= FLAG_LABEL_ORDER
     if o.recompute:
         flags |= FLAG_RECOMPUTE
+    if o.no_degree_bound:
+        flags |= FLAG_NO_DEGREE_BOUND
     c.flags = flags
     if o.observer is not None and keep is not None:
         obs = o.observer

@@ -35,6 +35,7 @@ MODES = {
     "label": (dict(label_order=True), None, {}),
     "recompute": (dict(recompute=True), None, {}),
     "inc": ({}, None, {}),
+    "inc_nobound": (dict(no_degree_bound=True), None, {}),
     "delta": ({}, "1e9", {}),
     "delta_host": (dict(host_loop=True), "1e9", dict(time_support=True)),
 }
