@@ -17,13 +17,19 @@ e.reset()
 tri = e.support_pass()
 print(f"support pass: T={tri} maxS={e.info()['max_support']}", flush=True)
 out = {"scale": scale, "n": g.num_vertices, "m": g.num_edges, "triangles": tri, "max_support": e.info()["max_support"]}
-for k in (3,):
+for k in (3, 10, 100, 935):
     e.reset(); h = e.run(k)
     ms = []
     for _ in range(2):
         e.reset(); h = e.run(k); ms.append(e.info()["device_ms"])
-    print(f"K={k}: rounds={len(h)} hist={h[:3]} ms={min(ms):.1f} survivors={e.info()['live_edges']}", flush=True)
+    print(f"K={k}: rounds={len(h)} hist={h[:3]} ms={min(ms):.1f} survivors={e.info()['live_edges']} T={e.info()['triangles']}", flush=True)
     out[f"k{k}_ms"] = min(ms); out[f"k{k}_hist"] = h; out[f"k{k}_survivors"] = e.info()["live_edges"]
+er = kt.Engine(g, kt.TrussOptions(recompute=True))
+for k in (3, 935):
+    er.reset(); hr = er.run(k)
+    print(f"recompute K={k}: rounds={len(hr)} ms={er.info()['device_ms']:.1f} survivors={er.info()['live_edges']}", flush=True)
+    out[f"k{k}_recompute_ms"] = er.info()["device_ms"]
+er.close()
 t = time.time()
 km = e.kmax()
 print(f"kmax={km} ({time.time()-t:.1f}s) survivors={e.info()['live_edges']}", flush=True)
@@ -31,7 +37,8 @@ e.reset(); h = e.run(km)
 print(f"K_max fixpoint: rounds={len(h)} ms={e.info()['device_ms']:.1f}", flush=True)
 out.update({"kmax": km, "kmax_rounds": len(h), "kmax_ms": e.info()["device_ms"], "kmax_survivors": e.info()["live_edges"]})
 e.close()
-ew = kt.Engine(g, collect_work=True); et = kt.Engine(g, time_support=True)
+ew = kt.Engine(g, kt.TrussOptions(recompute=True), collect_work=True)
+et = kt.Engine(g, kt.TrussOptions(recompute=True), time_support=True)
 for k in (3, km):
     ew.reset(); ew.run(k); w = ew.round_work(); et.reset(); et.run(k); tw = et.round_work()
     B = sum(4*x["L"] + 4*g.total_slots() + 4*(g.num_vertices+2) + 12*x["triangles"] for x in w)
