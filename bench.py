@@ -283,10 +283,10 @@ def main():
     for k in mine:
         eng.reset()
         h = eng.run(k)
-        # k_set_live + k_begin + 14 per round (plan x2, support, mark x2, decide,
+        # k_set_live + k_begin + 12 per round (A22-staged support, mark x2, decide,
         # queues, delta, rows x2, sym x2, zero, control; the ones a round does
         # not need exit at once) + 2 triangle total + 4 publish
-        launches_per_k[k] = 2 + 14 * len(h) + 2 + 4
+        launches_per_k[k] = 2 + 12 * len(h) + 2 + 4
         rounds_per_k[k] = len(h)
         live_per_k[k] = eng.info()["live_edges"]
 
@@ -500,9 +500,9 @@ def run_fixpoint_mode(args):
         kd.engine_join(eng)
     eng.reset()
     hist = eng.run(k)
-    # carried-support rounds on one rank (14 launches per round + 2 + 4);
+    # carried-support rounds on one rank (12 launches per round + 2 + 4);
     # the partitioned multi-rank loop recomputes (6 per round + 5 publish)
-    launches = (2 + 14 * len(hist) + 2 + 4) if world == 1 else (2 + 6 * len(hist) + 5)
+    launches = (2 + 12 * len(hist) + 2 + 4) if world == 1 else (2 + 6 * len(hist) + 5)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     for _ in range(args.warmup):
         eng.reset()

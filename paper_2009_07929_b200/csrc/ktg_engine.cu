@@ -171,6 +171,15 @@ struct ktg_engine {
   DBuf<uint8_t> dead, rdirty, sdirty;
   DBuf<uint4> rq;
   uint64_t sym_entries = 0, rq_cap = 0;
+  // A22-staged support pass: in-edge ids by j, their offsets, chunk first
+  // rows, (chunk, batch) tasks
+  DBuf<uint32_t> a22_pe, a22_off, a22_jfirst, a22_cnt;
+  DBuf<uint2> a22_tasks;
+  uint32_t a22_ntasks = 0;
+  bool a22_ready = false;
+  bool a22_off_env = false;   // KTG_SUPPORT=chunked: keep k_support_chunked in carried runs
+  int a22_grid = 0;
+  size_t a22_smem = 0;
   bool sym_ready = false;
   bool inc_active = false;    // the current fixpoint carries supports
   bool pristine = false;      // the working layout holds the pristine graph (after load / reset)
@@ -257,7 +266,8 @@ struct ktg_engine {
     orig_ids.release();
     cub_tmp.release();
     for (DBuf<uint32_t>* b : {&sym_nbr, &sym_eid, &sym_nbr_p, &sym_eid_p, &sym_deg, &sym_deg_p, &pos_of, &pos_of_p,
-                              &erow, &qsym, &qrow, &fq0, &fq1, &sym_heavy})
+                              &erow, &qsym, &qrow, &fq0, &fq1, &sym_heavy, &a22_pe, &a22_off, &a22_jfirst,
+                              &a22_cnt})
       b->release();
     sym_ptr.release();
     sym_sizes.release();
@@ -265,7 +275,9 @@ struct ktg_engine {
     rdirty.release();
     sdirty.release();
     rq.release();
+    a22_tasks.release();
     sym_ready = false;
+    a22_ready = false;
   }
 };
 
@@ -326,6 +338,12 @@ ktg_status engine_init(const ktg_options* opt, ktg_engine* e) {
   KTG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_p, k_prune_light<0>, kPruneThreads, 0));
   e->prune_grid = std::max(1, per_sm_p) * e->num_sms;
   e->heavy_grid = 2 * e->num_sms;
+  e->a22_smem = sizeof(A22Smem);
+  KTG_CUDA(cudaFuncSetAttribute(k_support_a22, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->a22_smem));
+  int per_sm_a = 0;
+  KTG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_a, k_support_a22, kSupportThreads, e->a22_smem));
+  e->a22_grid = std::max(1, per_sm_a) * e->num_sms;
+  if (const char* v = getenv("KTG_SUPPORT")) e->a22_off_env = std::string(v) == "chunked";
   return KTG_OK;
 }
 
@@ -446,6 +464,42 @@ ktg_status build_working(ktg_engine* e) {
   return prepare_layout(e, W, true);
 }
 
+// Static structures of the A22-staged support pass (after build_sym): the
+// pristine in-lists as edge ids, each chunk's first row, (chunk, batch) tasks.
+ktg_status build_a22(ktg_engine* e) {
+  Layout& W = e->wl;
+  const uint32_t n = W.n;
+  const uint64_t m = W.live_pristine;
+  const size_t nb = (size_t)n + 2;
+  const uint32_t Q = W.nchunks;
+  const cudaStream_t s = e->stream;
+  e->a22_ready = false;
+  KTG_TRY(e->a22_pe.ensure(m));
+  KTG_TRY(e->a22_off.ensure(nb));
+  KTG_TRY(e->a22_jfirst.ensure(Q));
+  KTG_TRY(e->a22_cnt.ensure((size_t)Q + 1));
+  Sym y = e->sym();
+  k_a22_pe<<<e->prune_grid, kPruneThreads, 0, s>>>(y, e->sym_sizes.p + 3 * nb, e->din.p, n, e->a22_pe.p,
+                                                   e->a22_off.p);
+  k_chunk_first<<<(Q + 255) / 256, 256, 0, s>>>(W.row_ptr.p, n, W.slots, Q, e->a22_jfirst.p);
+  k_a22_count<<<(Q + 256) / 256, 256, 0, s>>>(e->a22_jfirst.p, W.chunk_row.p, e->a22_off.p, Q, e->a22_cnt.p);
+  KTG_CUDA(cudaGetLastError());
+  size_t tmp = 0;
+  KTG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, e->a22_cnt.p, e->a22_cnt.p, (int)Q + 1, s));
+  KTG_TRY(e->cub_tmp.ensure(tmp));
+  tmp = e->cub_tmp.cap;
+  KTG_CUDA(cub::DeviceScan::ExclusiveSum(e->cub_tmp.p, tmp, e->a22_cnt.p, e->a22_cnt.p, (int)Q + 1, s));
+  uint32_t total = 0;
+  KTG_CUDA(cudaMemcpyAsync(&total, e->a22_cnt.p + Q, 4, cudaMemcpyDeviceToHost, s));
+  KTG_CUDA(cudaStreamSynchronize(s));
+  KTG_TRY(e->a22_tasks.ensure(std::max<uint32_t>(total, 1)));
+  k_a22_fill<<<(Q + 255) / 256, 256, 0, s>>>(e->a22_cnt.p, Q, e->a22_tasks.p);
+  KTG_CUDA(cudaGetLastError());
+  e->a22_ntasks = total;
+  e->a22_ready = true;
+  return KTG_OK;
+}
+
 // Symmetric adjacency of the (pristine) working layout for incremental
 // rounds: row v = sorted in-neighbours ++ out-neighbours (working row v), each
 // with the edge id; pos_of; pristine copies; the delta queue.
@@ -529,6 +583,7 @@ ktg_status build_sym(ktg_engine* e) {
   KTG_TRY(e->rq.ensure(cap));
   e->sym_ready = true;
   e->pristine = true;
+  return build_a22(e);
   return KTG_OK;
 }
 
@@ -698,10 +753,16 @@ ktg_status enqueue_round(ktg_engine* e, bool graph_mode, cudaGraphConditionalHan
   Graph g = e->graph_of(L);
   const cudaStream_t s = e->stream;
   const int fused = graph_mode ? 1 : 0;
-  k_plan_count<<<(L.nchunks + 255) / 256, 256, 0, s>>>(g, 0);
-  k_plan_write<<<1, 1024, 0, s>>>(g);
+  const bool a22 = e->inc_active && e->a22_ready && !e->a22_off_env;
+  if (!a22) {
+    k_plan_count<<<(L.nchunks + 255) / 256, 256, 0, s>>>(g, 0);
+    k_plan_write<<<1, 1024, 0, s>>>(g);
+  }
   if (sup0) KTG_CUDA(cudaEventRecord(sup0, s));
-  if (flag(e, KTG_FLAG_NAIVE_SUPPORT)) {
+  if (a22) {
+    A22 a{e->a22_pe.p, e->a22_off.p, e->a22_jfirst.p, e->a22_tasks.p, e->a22_ntasks};
+    k_support_a22<<<e->a22_grid, kSupportThreads, e->a22_smem, s>>>(g, e->sym(), a);
+  } else if (flag(e, KTG_FLAG_NAIVE_SUPPORT)) {
     k_support_naive<<<4 * e->num_sms, 256, 0, s>>>(g);
   } else {
     k_support_chunked<<<e->support_grid, kSupportThreads, e->support_smem, s>>>(g);

@@ -696,6 +696,304 @@ k_support_chunked(Graph g) {
   if (lane == 0 && tri_local) atomicAdd(&g.st->triangles, tri_local);
 }
 
+// ---------------------------------------------------------------------------
+// A22-staged support pass (working layout with the symmetric adjacency)
+// ---------------------------------------------------------------------------
+// The same triangles and increments as k_support_chunked, enumerated from the
+// other side. In degree order the a12 tails are the short side of almost
+// every intersection (R-MAT s20: sum of tails 1.23e9 against 4.42e9 A22-row
+// elements), so a task stages a 512-slot chunk of A22 rows N+(j) in shared
+// memory -- hashed by (value, row run) -- and streams the tail of every pivot
+// (i, j) whose j has a run in the chunk, probing each tail element once.
+// Pivots come from a static in-edge list (edge ids grouped by j); the
+// current slot of a pivot is pos_of[id] and dead ids are skipped, so the list
+// never needs rebuilding as rounds prune. A triangle (i, j, c) adds 1 to the
+// A22 slot (j, c) and the pivot (i, j) in shared memory and red.adds the tail
+// slot (i, c) once. Tasks are (chunk, batch of kA22Batch pivots), static.
+constexpr int kA22Batch = 256;
+
+struct A22 {
+  const uint32_t* pe;        // in-edge ids, grouped by j (pristine in-lists)
+  const uint32_t* pin_off;   // n+2: start of j's in-list in pe
+  const uint32_t* jfirst;    // per chunk: row holding the chunk's first slot
+  const uint2* tasks;        // (chunk, batch)
+  uint32_t ntasks;
+};
+
+struct A22Smem {
+  uint32_t A[kChunk];
+  uint32_t cntA[kChunk];
+  uint16_t nz[kChunk];
+  uint32_t rte[kChunk + 2];          // per row of the chunk: run [tb, te) as tb << 16 | te, or ~0
+  uint32_t roff[kChunk + 2];         // pin_off of the chunk's rows (+1)
+  uint32_t ps[kA22Batch];            // pivot slot (i, j)
+  uint32_t plo[kA22Batch];           // first tail slot probed
+  uint32_t prun[kA22Batch];          // j's run tb << 16 | te
+  uint32_t cntP[kA22Batch];
+  uint32_t pref[kA22Batch + 1];
+  __align__(16) uint32_t hkey[kBuckets][8];
+  __align__(16) uint32_t hmeta[kBuckets][8];
+  uint32_t hcnt[kBuckets];
+  uint32_t skey[kStash], smeta[kStash];
+  uint32_t nstash;
+  uint32_t red[kSupportThreads / 32];
+  uint32_t task;
+  uint32_t next;
+};
+
+__global__ void __launch_bounds__(kSupportThreads)
+k_support_a22(Graph g, Sym y, A22 a) {
+  if (g.st->mode) return;  // supports carried this round
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  A22Smem& s = *reinterpret_cast<A22Smem*>(smem_raw);
+  const uint32_t tid = threadIdx.x;
+  const int lane = tid & 31, wid = tid >> 5;
+  constexpr int NW = kSupportThreads / 32;
+  constexpr int EPT = kChunk / kSupportThreads;
+  uint32_t* __restrict__ S = cur_S(g);
+  const uint32_t* __restrict__ col = g.col;
+  const uint32_t h0 = g.st->h0;
+  unsigned long long tri_local = 0;
+
+  for (;;) {
+    if (tid == 0) {
+      s.task = atomicAdd(&g.st->task_next, 1u);
+      s.next = 0;
+      s.nstash = 0;
+    }
+    __syncthreads();
+    const uint32_t t = s.task;
+    if (t >= a.ntasks) break;
+    const uint2 tk = a.tasks[a.ntasks - 1 - t];  // dense (high-rank) chunks first
+    const uint32_t q = tk.x;
+    const uint64_t a0 = (uint64_t)q * kChunk;
+    const uint32_t alen = (uint32_t)umin64(kChunk, g.slots - a0);
+    const uint32_t jf = a.jfirst[q], jl = g.chunk_row[q];
+    const uint32_t nrows = jl - jf + 1;
+
+    // 1. rows of the chunk (live run inside the chunk, in-list offsets) and
+    //    the batch's pivot descriptors, before anything is staged: batches
+    //    whose pivots are all dead cost only this
+    for (uint32_t r = tid; r <= nrows; r += kSupportThreads) {
+      const uint32_t j = jf + r;
+      s.roff[r] = a.pin_off[j];
+      if (r < nrows) {
+        const uint64_t rb = g.row_ptr[j], re = rb + g.deg[j];
+        const uint64_t lo = rb > a0 ? rb : a0, hi = re < a0 + alen ? re : a0 + alen;
+        s.rte[r] = (lo < hi && j >= h0 && j != 0) ? (uint32_t)((lo - a0) << 16 | (hi - a0)) : 0xffffffffu;
+      }
+    }
+    __syncthreads();
+
+    // 2. pivot descriptors of this batch: slot, tail (clipped to the run's
+    //    value range when j's row continues outside the chunk)
+    const uint32_t k0 = s.roff[0] + tk.y * kA22Batch;
+    const uint32_t k1 = min(k0 + kA22Batch, s.roff[nrows]);
+    uint32_t cost = 0;
+    s.cntP[tid] = 0;
+    if (k0 + tid < k1) {
+      const uint32_t k = k0 + tid;
+      // row of pivot k: last r with roff[r] <= k
+      uint32_t lo = 0, hi = nrows;
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (s.roff[mid] <= k) lo = mid; else hi = mid;
+      }
+      const uint32_t run = s.rte[lo];
+      const uint32_t id = a.pe[k];
+      if (run != 0xffffffffu && !y.dead[id]) {
+        const uint32_t ps = y.pos_of[id];
+        const uint32_t i = y.erow[id];
+        const uint32_t iend = g.row_ptr[i] + g.deg[i];
+        uint32_t tlo = ps + 1, thi = iend;
+        const uint32_t tb = run >> 16, te = run & 0xffffu;
+        const uint32_t j = jf + lo;
+        const uint64_t rb = g.row_ptr[j];
+        if (rb < a0 || rb + g.deg[j] > a0 + alen) {  // partial run: clip the tail
+          tlo = lb_global(col, tlo, thi, col[a0 + tb]);
+          thi = lb_global(col, tlo, thi, col[a0 + te - 1] + 1);
+        }
+        if (thi > tlo) {
+          cost = thi - tlo;
+          s.ps[tid] = ps;
+          s.plo[tid] = tlo;
+          s.prun[tid] = run;
+        }
+      }
+    }
+    uint32_t W;
+    const uint32_t run0 = block_exscan(cost, s.red, &W);
+    s.pref[tid] = run0;
+    if (tid == 0) s.pref[kA22Batch] = W;
+    if (W == 0) continue;  // no live pivot reaches this chunk (uniform; nothing staged yet)
+
+    // 3. stage the chunk, next zeros, (value, run end) hash -- as k_support_chunked
+    for (uint32_t b = tid; b < (uint32_t)kBuckets; b += kSupportThreads) {
+      s.hcnt[b] = 0;
+#pragma unroll
+      for (int e = 0; e < 8; ++e) s.hkey[b][e] = 0;
+    }
+    uint32_t first_zero = 0xffffffffu;
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      const uint32_t x = tid * EPT + e;
+      const uint32_t v = x < alen ? col[a0 + x] : 0u;
+      s.A[x] = v;
+      s.cntA[x] = 0;
+      if (v == 0 && x < alen && first_zero == 0xffffffffu) first_zero = x;
+    }
+    {
+      uint32_t m = first_zero;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_down_sync(0xffffffffu, m, o);
+        if (lane + o < 32) m = min(m, v);
+      }
+      if (lane == 0) s.red[wid] = m;
+      __syncthreads();
+      uint32_t carry = 0xffffffffu;
+      for (int w = wid + 1; w < NW; ++w) carry = min(carry, s.red[w]);
+      const uint32_t incl_next = __shfl_down_sync(0xffffffffu, m, 1);
+      if (lane < 31) carry = min(carry, incl_next);
+      uint32_t cur = min(carry, alen);
+#pragma unroll
+      for (int e = EPT - 1; e >= 0; --e) {
+        const uint32_t x = tid * EPT + e;
+        const uint32_t v = s.A[x];
+        if (x < alen && v == 0) cur = x;
+        s.nz[x] = (uint16_t)min(cur, (uint32_t)kChunk);
+        if (v != 0) {
+          const uint32_t b = bucket_of(v, cur);
+          const uint32_t at = atomicAdd(&s.hcnt[b], 1u);
+          const uint32_t meta = (cur << 16) | x;
+          if (at < 8) {
+            s.hkey[b][at] = v;
+            s.hmeta[b][at] = meta;
+          } else {
+            const uint32_t z = atomicAdd(&s.nstash, 1u);
+            if (z < kStash) {
+              s.skey[z] = v;
+              s.smeta[z] = meta;
+            }
+          }
+        }
+      }
+    }
+    __syncthreads();
+
+    // 4. flattened tail elements, strips grabbed dynamically by warps
+    for (;;) {
+      uint32_t base = 0;
+      if (lane == 0) base = atomicAdd(&s.next, (uint32_t)kStrip);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (base >= W) break;
+      const uint32_t lim = min(base + (uint32_t)kStrip, W);
+      uint32_t p;
+      {
+        uint32_t lo = 0, hi = kA22Batch;
+        while (lo < hi) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (s.pref[mid + 1] <= base) lo = mid + 1; else hi = mid;
+        }
+        p = lo;
+      }
+      uint32_t pe_ = s.pref[p + 1], pb = s.pref[p], plo = s.plo[p], prun = s.prun[p];
+      for (uint32_t f = base + lane; f < lim; f += 32) {
+        if (f >= pe_) {
+          do {
+            ++p;
+            pe_ = s.pref[p + 1];
+          } while (pe_ <= f);
+          pb = s.pref[p];
+          plo = s.plo[p];
+          prun = s.prun[p];
+        }
+        const uint32_t slot = plo + (f - pb);
+        const uint32_t c = col[slot];
+        const uint32_t tb = prun >> 16, te = prun & 0xffffu;
+        uint32_t x;
+        if (s.nstash <= (uint32_t)kStash) {
+          x = hash_find(s, c, tb, te);
+        } else {
+          x = tb + lb_smem(s.A + tb, te - tb, c);
+          if (!(x < te && s.A[x] == c)) x = kChunk;
+        }
+        if (x < (uint32_t)kChunk) {
+          atomicAdd(&s.cntA[x], 1u);
+          atomicAdd(&S[slot], 1u);
+          atomicAdd(&s.cntP[p], 1u);
+          ++tri_local;
+        }
+      }
+    }
+    __syncthreads();
+
+    // 5. flush shared counts (A22 slots, pivots)
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      const uint32_t x = tid * EPT + e;
+      const uint32_t ca = s.cntA[x];
+      if (ca) atomicAdd(&S[a0 + x], ca);
+    }
+    {
+      const uint32_t cp = s.cntP[tid];
+      if (cp) atomicAdd(&S[s.ps[tid]], cp);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) tri_local += __shfl_xor_sync(0xffffffffu, tri_local, o);
+  if (lane == 0 && tri_local) atomicAdd(&g.st->triangles, tri_local);
+}
+
+// Load time: row holding each chunk's first slot.
+__global__ void k_chunk_first(const uint32_t* __restrict__ row_ptr, uint32_t n, uint64_t slots, uint32_t nchunks,
+                              uint32_t* __restrict__ jfirst) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nchunks) return;
+  const uint32_t e = (uint32_t)((uint64_t)q * kChunk);
+  uint32_t lo = 0, hi = n + 2;
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (row_ptr[mid] <= e) lo = mid + 1; else hi = mid;
+  }
+  jfirst[q] = max(lo - 1, 1u);
+}
+
+// Load time: batches per chunk (pivots into the chunk's rows / kA22Batch).
+__global__ void k_a22_count(const uint32_t* __restrict__ jfirst, const uint32_t* __restrict__ chunk_row,
+                            const uint32_t* __restrict__ pin_off, uint32_t nchunks, uint32_t* __restrict__ cnt) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q > nchunks) return;
+  if (q == nchunks) {
+    cnt[q] = 0;
+    return;
+  }
+  const uint32_t k0 = pin_off[jfirst[q]], k1 = pin_off[chunk_row[q] + 1];
+  cnt[q] = (k1 - k0 + kA22Batch - 1) / kA22Batch;
+}
+
+__global__ void k_a22_fill(const uint32_t* __restrict__ cnt_off, uint32_t nchunks, uint2* __restrict__ tasks) {
+  const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
+  if (q >= nchunks) return;
+  const uint32_t o = cnt_off[q], c = cnt_off[q + 1] - o;
+  for (uint32_t b = 0; b < c; ++b) tasks[o + b] = make_uint2(q, b);
+}
+
+// Load time: the in-part of every pristine symmetric row (edge ids), packed.
+__global__ void k_a22_pe(Sym y, const unsigned long long* __restrict__ inoff, const uint32_t* __restrict__ din,
+                         uint32_t n, uint32_t* __restrict__ pe, uint32_t* __restrict__ pin_off) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  for (uint32_t v = warp; v <= n + 1; v += nwarps) {
+    const unsigned long long o = inoff[v], b = y.ptr[v];
+    if (lane == 0) pin_off[v] = (uint32_t)o;
+    if (v == 0 || v > n) continue;
+    for (uint32_t x = lane; x < din[v]; x += 32) pe[o + x] = y.eid[b + x];
+  }
+}
+
 // Paper Listing 1 / support.cpp:115-127 as written: one thread per slot,
 // sequential two-pointer merge. Cross-check kernel only.
 __global__ void k_support_naive(Graph g) {
