@@ -711,6 +711,8 @@ k_support_chunked(Graph g) {
 // A22 slot (j, c) and the pivot (i, j) in shared memory and red.adds the tail
 // slot (i, c) once. Tasks are (chunk, batch of kA22Batch pivots), static.
 constexpr int kA22Batch = 256;
+constexpr int kA22TableBits = 11;          // 2048 slots for <= 512 entries (load <= 0.25)
+constexpr int kA22Table = 1 << kA22TableBits;
 
 struct A22 {
   const uint32_t* pe;        // in-edge ids, grouped by j (pristine in-lists)
@@ -731,15 +733,15 @@ struct A22Smem {
   uint32_t prun[kA22Batch];          // j's run tb << 16 | te
   uint32_t cntP[kA22Batch];
   uint32_t pref[kA22Batch + 1];
-  __align__(16) uint32_t hkey[kBuckets][8];
-  __align__(16) uint32_t hmeta[kBuckets][8];
-  uint32_t hcnt[kBuckets];
-  uint32_t skey[kStash], smeta[kStash];
-  uint32_t nstash;
+  uint2 tab[kA22Table];              // open addressing: {value (0 = empty), chunk position}
   uint32_t red[kSupportThreads / 32];
   uint32_t task;
   uint32_t next;
 };
+
+__device__ __forceinline__ uint32_t a22_hash(uint32_t v, uint32_t te) {
+  return ((v ^ (te * 0x85EBCA6Bu)) * 2654435761u) >> (32 - kA22TableBits);
+}
 
 __global__ void __launch_bounds__(kSupportThreads)
 k_support_a22(Graph g, Sym y, A22 a) {
@@ -759,7 +761,6 @@ k_support_a22(Graph g, Sym y, A22 a) {
     if (tid == 0) {
       s.task = atomicAdd(&g.st->task_next, 1u);
       s.next = 0;
-      s.nstash = 0;
     }
     __syncthreads();
     const uint32_t t = s.task;
@@ -828,11 +829,7 @@ k_support_a22(Graph g, Sym y, A22 a) {
     if (W == 0) continue;  // no live pivot reaches this chunk (uniform; nothing staged yet)
 
     // 3. stage the chunk, next zeros, (value, run end) hash -- as k_support_chunked
-    for (uint32_t b = tid; b < (uint32_t)kBuckets; b += kSupportThreads) {
-      s.hcnt[b] = 0;
-#pragma unroll
-      for (int e = 0; e < 8; ++e) s.hkey[b][e] = 0;
-    }
+    for (uint32_t b = tid; b < (uint32_t)kA22Table; b += kSupportThreads) s.tab[b] = make_uint2(0, 0);
     uint32_t first_zero = 0xffffffffu;
 #pragma unroll
     for (int e = 0; e < EPT; ++e) {
@@ -862,20 +859,10 @@ k_support_a22(Graph g, Sym y, A22 a) {
         const uint32_t v = s.A[x];
         if (x < alen && v == 0) cur = x;
         s.nz[x] = (uint16_t)min(cur, (uint32_t)kChunk);
-        if (v != 0) {
-          const uint32_t b = bucket_of(v, cur);
-          const uint32_t at = atomicAdd(&s.hcnt[b], 1u);
-          const uint32_t meta = (cur << 16) | x;
-          if (at < 8) {
-            s.hkey[b][at] = v;
-            s.hmeta[b][at] = meta;
-          } else {
-            const uint32_t z = atomicAdd(&s.nstash, 1u);
-            if (z < kStash) {
-              s.skey[z] = v;
-              s.smeta[z] = meta;
-            }
-          }
+        if (v != 0) {  // claim the first free slot from home (values are >= 1)
+          uint32_t h = a22_hash(v, cur);
+          while (atomicCAS(&s.tab[h].x, 0u, v) != 0u) h = (h + 1) & (kA22Table - 1);
+          s.tab[h].y = x;
         }
       }
     }
@@ -911,12 +898,15 @@ k_support_a22(Graph g, Sym y, A22 a) {
         const uint32_t slot = plo + (f - pb);
         const uint32_t c = col[slot];
         const uint32_t tb = prun >> 16, te = prun & 0xffffu;
-        uint32_t x;
-        if (s.nstash <= (uint32_t)kStash) {
-          x = hash_find(s, c, tb, te);
-        } else {
-          x = tb + lb_smem(s.A + tb, te - tb, c);
-          if (!(x < te && s.A[x] == c)) x = kChunk;
+        // (value, run) lookup: the value may also sit in other rows' runs
+        uint32_t x = kChunk;
+        for (uint32_t h = a22_hash(c, te);; h = (h + 1) & (kA22Table - 1)) {
+          const uint2 e = s.tab[h];
+          if (e.x == 0) break;
+          if (e.x == c && e.y >= tb && e.y < te) {
+            x = e.y;
+            break;
+          }
         }
         if (x < (uint32_t)kChunk) {
           atomicAdd(&s.cntA[x], 1u);
