@@ -174,7 +174,7 @@ struct ktg_engine {
   // A22-staged support pass: in-edge ids by j, their offsets, chunk first
   // rows, (chunk, batch) tasks
   DBuf<uint32_t> a22_pe, a22_off, a22_jfirst, a22_cnt;
-  DBuf<uint2> a22_tasks;
+  DBuf<uint2> a22_tasks, a22_pin;
   uint32_t a22_ntasks = 0;
   bool a22_ready = false;
   bool a22_off_env = false;   // KTG_SUPPORT=chunked: keep k_support_chunked in carried runs
@@ -276,6 +276,7 @@ struct ktg_engine {
     sdirty.release();
     rq.release();
     a22_tasks.release();
+    a22_pin.release();
     sym_ready = false;
     a22_ready = false;
   }
@@ -475,12 +476,14 @@ ktg_status build_a22(ktg_engine* e) {
   const cudaStream_t s = e->stream;
   e->a22_ready = false;
   KTG_TRY(e->a22_pe.ensure(m));
+  KTG_TRY(e->a22_pin.ensure(m));
   KTG_TRY(e->a22_off.ensure(nb));
   KTG_TRY(e->a22_jfirst.ensure(Q));
   KTG_TRY(e->a22_cnt.ensure((size_t)Q + 1));
   Sym y = e->sym();
   k_a22_pe<<<e->prune_grid, kPruneThreads, 0, s>>>(y, e->sym_sizes.p + 3 * nb, e->din.p, n, e->a22_pe.p,
                                                    e->a22_off.p);
+  k_a22_pin<<<4 * e->num_sms, 256, 0, s>>>(e->a22_pe.p, m, y, e->a22_pin.p);
   k_chunk_first<<<(Q + 255) / 256, 256, 0, s>>>(W.row_ptr.p, n, W.slots, Q, e->a22_jfirst.p);
   k_a22_count<<<(Q + 256) / 256, 256, 0, s>>>(e->a22_jfirst.p, W.chunk_row.p, e->a22_off.p, Q, e->a22_cnt.p);
   KTG_CUDA(cudaGetLastError());
@@ -760,7 +763,7 @@ ktg_status enqueue_round(ktg_engine* e, bool graph_mode, cudaGraphConditionalHan
   }
   if (sup0) KTG_CUDA(cudaEventRecord(sup0, s));
   if (a22) {
-    A22 a{e->a22_pe.p, e->a22_off.p, e->a22_jfirst.p, e->a22_tasks.p, e->a22_ntasks};
+    A22 a{e->a22_pe.p, e->a22_pin.p, e->a22_off.p, e->a22_jfirst.p, e->a22_tasks.p, e->a22_ntasks};
     k_support_a22<<<e->a22_grid, kSupportThreads, e->a22_smem, s>>>(g, e->sym(), a);
   } else if (flag(e, KTG_FLAG_NAIVE_SUPPORT)) {
     k_support_naive<<<4 * e->num_sms, 256, 0, s>>>(g);
@@ -873,8 +876,12 @@ ktg_status begin_run(ktg_engine* e, uint32_t k, int parity) {
   }
   k_begin<<<1, 1, 0, e->stream>>>(e->d_st, k >= 2 ? k - 2 : 0, e->opt.width_bits == 16 ? 1 : 0, parity,
                                   e->inc_active ? 1u : 0u, e->delta_ratio16);
-  if (e->inc_active && e->pristine && !flag(e, KTG_FLAG_NO_DEGREE_BOUND))
-    k_heavy_rank<<<1, 1, 0, e->stream>>>(e->d_st, e->sym_deg_p.p, e->wl.n);
+  if (e->inc_active && e->pristine) {
+    if (!flag(e, KTG_FLAG_NO_DEGREE_BOUND))
+      k_heavy_rank<<<1, 1, 0, e->stream>>>(e->d_st, e->sym_deg_p.p, e->wl.n);
+    else
+      k_set_pristine<<<1, 1, 0, e->stream>>>(e->d_st);
+  }
   e->pristine = false;
   KTG_CUDA(cudaGetLastError());
   return KTG_OK;

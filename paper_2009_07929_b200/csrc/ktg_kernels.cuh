@@ -61,6 +61,7 @@ struct DevState {
   unsigned int nqrow, nqsym;         // rows queued for compaction this round
   unsigned int nheavy_sym;           // long symmetric rows queued for CTA compaction
   unsigned int h0;                   // round 0 from pristine: first rank of degree >= k-1 (0: off)
+  unsigned int pristine;             // this round runs on the pristine working layout
 };
 
 struct Graph {
@@ -716,6 +717,7 @@ constexpr int kA22Table = 1 << kA22TableBits;
 
 struct A22 {
   const uint32_t* pe;        // in-edge ids, grouped by j (pristine in-lists)
+  const uint2* pin_p;        // the same pivots in the pristine graph: {slot, row i}
   const uint32_t* pin_off;   // n+2: start of j's in-list in pe
   const uint32_t* jfirst;    // per chunk: row holding the chunk's first slot
   const uint2* tasks;        // (chunk, batch)
@@ -755,6 +757,7 @@ k_support_a22(Graph g, Sym y, A22 a) {
   uint32_t* __restrict__ S = cur_S(g);
   const uint32_t* __restrict__ col = g.col;
   const uint32_t h0 = g.st->h0;
+  const bool pristine = g.st->pristine;
   unsigned long long tri_local = 0;
 
   for (;;) {
@@ -801,10 +804,19 @@ k_support_a22(Graph g, Sym y, A22 a) {
         if (s.roff[mid] <= k) lo = mid; else hi = mid;
       }
       const uint32_t run = s.rte[lo];
-      const uint32_t id = a.pe[k];
-      if (run != 0xffffffffu && !y.dead[id]) {
-        const uint32_t ps = y.pos_of[id];
-        const uint32_t i = y.erow[id];
+      bool live = false;
+      uint32_t ps = 0, i = 0;
+      if (run != 0xffffffffu) {
+        if (pristine) {  // static {slot, row}: no dead / pos_of / erow gathers
+          const uint2 pv = a.pin_p[k];
+          ps = pv.x, i = pv.y, live = true;
+        } else {
+          const uint32_t id = a.pe[k];
+          live = !y.dead[id];
+          if (live) ps = y.pos_of[id], i = y.erow[id];
+        }
+      }
+      if (live) {
         const uint32_t iend = g.row_ptr[i] + g.deg[i];
         uint32_t tlo = ps + 1, thi = iend;
         const uint32_t tb = run >> 16, te = run & 0xffffu;
@@ -934,6 +946,14 @@ k_support_a22(Graph g, Sym y, A22 a) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) tri_local += __shfl_xor_sync(0xffffffffu, tri_local, o);
   if (lane == 0 && tri_local) atomicAdd(&g.st->triangles, tri_local);
+}
+
+// Load time: pristine {slot, row} of every pivot of the in-edge list.
+__global__ void k_a22_pin(const uint32_t* __restrict__ pe, uint64_t m, Sym y, uint2* __restrict__ pin_p) {
+  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < m; k += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t id = pe[k];
+    pin_p[k] = make_uint2(y.pos_of[id], y.erow[id]);
+  }
 }
 
 // Load time: row holding each chunk's first slot.
@@ -1414,7 +1434,10 @@ __global__ void k_heavy_rank(DevState* st, const uint32_t* __restrict__ symdeg_p
     if (symdeg_p[mid] < need) lo = mid + 1; else hi = mid;
   }
   st->h0 = lo;
+  st->pristine = 1;
 }
+
+__global__ void k_set_pristine(DevState* st) { st->pristine = 1; }
 
 // One thread: this round's removal count is final; choose carry vs recompute.
 __global__ void k_decide(DevState* st) {
@@ -1772,6 +1795,7 @@ __global__ void k_control_inc(DevState* st, unsigned long long* hist, cudaGraphC
   st->live_cost = st->keep_cost;
   st->mode = st->carry;
   st->h0 = 0;  // round 0 only
+  st->pristine = 0;
   st->nfq[st->fpar] = 0;
   st->fpar ^= 1u;
   st->carry = 0;
@@ -2031,6 +2055,7 @@ __global__ void k_begin(DevState* st, uint32_t threshold, uint32_t width16, int 
   st->nqrow = st->nqsym = 0;
   st->nheavy_sym = 0;
   st->h0 = 0;
+  st->pristine = 0;
   st->live_cost = 0;
   st->delta_ratio16 = delta_ratio16;
   st->sum_s = 0;
