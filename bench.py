@@ -144,6 +144,14 @@ def support_bytes(w, n, slots):
     return 4 * w["L"] + 4 * slots + 4 * (n + 2) + 12 * w["triangles"]
 
 
+def executed_bytes(w, n, slots, m):
+    """Bytes k_support_a22 itself moves per launch: the a12 tails it streams
+    (4*L_tail), the staged A22 chunks (4*slots), the pivot records (8 per
+    live edge), row offsets/degrees (8*(n+2)) and 3 u32 atomics per
+    triangle."""
+    return 4 * w["L_tail"] + 4 * slots + 8 * m + 8 * (n + 2) + 12 * w["triangles"]
+
+
 def fixpoint_bytes(work, n, slots):
     """Per-fixpoint algorithmic bytes B of SURVEY.md §8(d) (support + the
     16 B/slot prune)."""
@@ -283,10 +291,10 @@ def main():
     for k in mine:
         eng.reset()
         h = eng.run(k)
-        # k_set_live + k_begin + 12 per round (A22-staged support, mark x2, decide,
+        # k_set_live + k_begin + 13 per round (A22-staged support, mark x2, decide,
         # queues, delta, rows x2, sym x2, zero, control; the ones a round does
         # not need exit at once) + 2 triangle total + 4 publish
-        launches_per_k[k] = 2 + 12 * len(h) + 2 + 4
+        launches_per_k[k] = 2 + 13 * len(h) + 2 + 4
         rounds_per_k[k] = len(h)
         live_per_k[k] = eng.info()["live_edges"]
 
@@ -370,11 +378,12 @@ def main():
         except Exception:
             peak, peak_src = 6650.0, "fallback"
         sample_k = sorted(set([ks[0]] + ks[len(ks) // 4::max(1, len(ks) // 4)] + [ks[-1]]))
-        # full support passes every round (recompute mode): each launch is a
-        # whole-graph pass whose algorithmic bytes are the §8(d) formula
-        ew = kt.Engine(g, kt.TrussOptions(recompute=True), collect_work=True)
-        et = kt.Engine(g, kt.TrussOptions(recompute=True), time_support=True)
-        tot_b = tot_ms = 0.0
+        # the headline path's support kernel (k_support_a22) on the rounds
+        # that run a full pass; no round-0 degree bound here, so every launch
+        # is a whole-graph pass whose algorithmic bytes are the §8(d) formula
+        ew = kt.Engine(g, kt.TrussOptions(no_degree_bound=True), collect_work=True)
+        et = kt.Engine(g, kt.TrussOptions(no_degree_bound=True), time_support=True)
+        tot_b = tot_ms = tot_x = 0.0
         n_launch = 0
         fix_b = 0.0
         for k in sample_k:
@@ -388,6 +397,7 @@ def main():
                 if not t["full_pass"]:  # supports carried: the launch exits at once
                     continue
                 tot_b += support_bytes(w, n, slots)
+                tot_x += executed_bytes(w, n, slots, w["live_edges"])
                 tot_ms += t["support_ms"]
                 n_launch += 1
             fix_b += fixpoint_bytes(work, n, slots)
@@ -404,10 +414,15 @@ def main():
                 traffic = None
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic,
-                "peak_source": peak_src, "kernel": "k_support_chunked",
+                "peak_source": peak_src, "kernel": "k_support_a22",
                 "launches_measured": n_launch, "sample_k": sample_k,
                 "bytes_per_launch_avg": tot_b / max(1, n_launch),
-                "ms_per_launch_avg": tot_ms / max(1, n_launch)}
+                "ms_per_launch_avg": tot_ms / max(1, n_launch),
+                "executed_bytes_per_launch_avg": tot_x / max(1, n_launch),
+                "executed_frac": round(tot_x / (tot_ms / 1e3) / 1e9 / peak, 4),
+                "note": "achieved = SURVEY §8(d) algorithmic bytes (full merge view, 4 B per list element of "
+                        "L) / time; the kernel itself reads only the a12 tails (executed bytes = "
+                        "4*L_tail + 4*slots staged + 8*m pivot records + 12*T)"}
 
     # ---- CPU baseline: the reference library on the host cores ----
     cpu = None
@@ -500,9 +515,9 @@ def run_fixpoint_mode(args):
         kd.engine_join(eng)
     eng.reset()
     hist = eng.run(k)
-    # carried-support rounds on one rank (12 launches per round + 2 + 4);
+    # carried-support rounds on one rank (13 launches per round + 2 + 4);
     # the partitioned multi-rank loop recomputes (6 per round + 5 publish)
-    launches = (2 + 12 * len(hist) + 2 + 4) if world == 1 else (2 + 6 * len(hist) + 5)
+    launches = (2 + 13 * len(hist) + 2 + 4) if world == 1 else (2 + 6 * len(hist) + 5)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     for _ in range(args.warmup):
         eng.reset()
@@ -550,8 +565,11 @@ def run_fixpoint_mode(args):
             peak, src = 6650.0, "fallback"
         # full support passes every round (recompute mode): each launch is a
         # whole-graph pass whose algorithmic bytes are the §8(d) formula
-        ew = kt.Engine(g, kt.TrussOptions(recompute=True), collect_work=True)
-        et = kt.Engine(g, kt.TrussOptions(recompute=True), time_support=True)
+        # one rank: the carried-support path's k_support_a22 (full-pass rounds,
+        # no round-0 degree bound); ranks > 1 recompute with k_support_chunked
+        ro = kt.TrussOptions(no_degree_bound=True) if world == 1 else kt.TrussOptions(recompute=True)
+        ew = kt.Engine(g, ro, collect_work=True)
+        et = kt.Engine(g, ro, time_support=True)
         ew.reset(); ew.run(k); w = ew.round_work()
         et.reset(); et.run(k); tw = et.round_work()
         ew.close(); et.close()
@@ -561,7 +579,8 @@ def run_fixpoint_mode(args):
         achieved = tb / (tm / 1e3) / 1e9
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": None, "peak_source": src,
-                "kernel": "k_support_chunked", "launches_measured": len(full)}
+                "kernel": "k_support_a22" if world == 1 else "k_support_chunked",
+                "launches_measured": len(full)}
         if world == 1 and not args.no_cpu_baseline:
             v, desc = cpu_port_sample(g, k, args.cpu_budget_s, 1)
             cpu = {"value": v, "unit": "edges/s", "cores": 1, "kind": "port", "sample": desc}

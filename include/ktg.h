@@ -191,6 +191,7 @@ typedef struct {
   uint32_t full_pass;   /* 1: the round ran a full support pass; 0: its
                            supports were carried from the previous round */
   uint32_t pad;
+  uint64_t L_tail;      /* the a12-tail part of L: sum_v d+(d+-1)/2       */
 } ktg_round_work;
 
 ktg_status ktg_engine_create(const ktg_options* opt, ktg_engine** out);

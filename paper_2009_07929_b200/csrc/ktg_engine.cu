@@ -320,7 +320,7 @@ ktg_status engine_init(const ktg_options* opt, ktg_engine* e) {
   KTG_CUDA(cudaMalloc(&e->d_st, sizeof(DevState)));
   KTG_CUDA(cudaMemset(e->d_st, 0, sizeof(DevState)));
   KTG_CUDA(cudaMalloc(&e->d_hist, sizeof(unsigned long long) * kHistCap));
-  KTG_CUDA(cudaMalloc(&e->d_workL, sizeof(unsigned long long)));
+  KTG_CUDA(cudaMalloc(&e->d_workL, 2 * sizeof(unsigned long long)));
   KTG_CUDA(cudaMallocHost(&e->h_st, sizeof(DevState)));
   std::memset(e->h_st, 0, sizeof(DevState));
   KTG_CUDA(cudaEventCreate(&e->ev0));
@@ -780,6 +780,7 @@ ktg_status enqueue_round(ktg_engine* e, bool graph_mode, cudaGraphConditionalHan
     k_decide<<<1, 1, 0, s>>>(e->d_st);
     k_queues<<<4 * e->num_sms, 256, 0, s>>>(g, y);
     k_delta<<<e->prune_grid, kPruneThreads, 0, s>>>(g, y);
+    k_delta_big<<<e->prune_grid, kPruneThreads, 0, s>>>(g, y);
     k_inc_rows<0><<<e->prune_grid, kPruneThreads, 0, s>>>(g, y);
     k_inc_rows<1><<<e->heavy_grid, kPruneThreads, 0, s>>>(g, y);
     k_inc_sym<0><<<e->prune_grid, kPruneThreads, 0, s>>>(g, y);
@@ -892,15 +893,16 @@ ktg_status collect_work(ktg_engine* e, ktg_round_work* w) {
   Graph g = e->graph_of(L);
   KTG_TRY(e->din.ensure((size_t)L.n + 2));
   KTG_CUDA(cudaMemsetAsync(e->din.p, 0, ((size_t)L.n + 2) * 4, e->stream));
-  KTG_CUDA(cudaMemsetAsync(e->d_workL, 0, 8, e->stream));
+  KTG_CUDA(cudaMemsetAsync(e->d_workL, 0, 16, e->stream));
   k_work_din<<<e->prune_grid, kPruneThreads, 0, e->stream>>>(g, e->din.p);
   k_work_L<<<4 * e->num_sms, 256, 0, e->stream>>>(g, e->din.p, e->d_workL);
   KTG_CUDA(cudaGetLastError());
-  unsigned long long L2 = 0, live = 0;
-  KTG_CUDA(cudaMemcpyAsync(&L2, e->d_workL, 8, cudaMemcpyDeviceToHost, e->stream));
+  unsigned long long L2[2] = {0, 0}, live = 0;
+  KTG_CUDA(cudaMemcpyAsync(L2, e->d_workL, 16, cudaMemcpyDeviceToHost, e->stream));
   KTG_CUDA(cudaMemcpyAsync(&live, &e->d_st->live, 8, cudaMemcpyDeviceToHost, e->stream));
   KTG_CUDA(cudaStreamSynchronize(e->stream));
-  w->L = L2;
+  w->L = L2[0];
+  w->L_tail = L2[1];
   w->live_edges = live;
   return KTG_OK;
 }

@@ -108,7 +108,7 @@ struct Sym {
 };
 
 constexpr uint32_t kDeadMark = 0x80000000u;  // col mark of an edge removed this round
-constexpr int kDeltaPiece = 256;             // smaller-list elements per delta task
+constexpr int kDeltaPiece = 64;              // smaller-list elements per delta task
 
 __host__ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
 
@@ -1270,36 +1270,15 @@ __device__ __forceinline__ void append_coalesced(uint32_t* cnt, uint32_t* q, uin
 }
 
 // Removal of edge id at working slot p = (u, v): col mark, dead flag, the
-// far endpoint's symmetric row flagged (the caller flags row u), delta
-// tasks. Flags are plain byte stores (every writer stores 1); k_queues turns
-// them into the compaction queues. Returns min(du, dv) (the delta cost).
+// far endpoint's symmetric row flagged (the caller flags row u). Flags are
+// plain byte stores (every writer stores 1); k_queues turns them into the
+// compaction queues. Returns min(du, dv) (the edge's delta cost).
 __device__ __forceinline__ uint32_t mark_removed(const Graph& g, const Sym& y, uint32_t p, uint32_t u, uint32_t v,
-                                                 uint32_t id, uint32_t* ntask) {
+                                                 uint32_t id) {
   g.col[p] = v | kDeadMark;
   y.dead[id] = 1;
   y.sdirty[v] = 1;
-  const uint32_t mn = min(y.deg[u], y.deg[v]);
-  *ntask = (mn + kDeltaPiece - 1) / kDeltaPiece;
-  return mn;
-}
-
-// Warp-aggregated append of ntask delta tasks {p, u, v, piece} per lane.
-__device__ __forceinline__ void push_tasks(const Graph& g, const Sym& y, uint32_t ntask, uint32_t p, uint32_t u,
-                                           uint32_t v) {
-  const int lane = threadIdx.x & 31;
-  const unsigned act = __activemask();
-  uint32_t incl = ntask;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const uint32_t t = __shfl_up_sync(act, incl, o);
-    if (lane >= o) incl += t;
-  }
-  const uint32_t total = __shfl_sync(act, incl, 31);
-  if (total == 0) return;
-  uint32_t at = 0;
-  if (lane == 31) at = atomicAdd(&g.st->nrq, total);
-  at = __shfl_sync(act, at, 31) + incl - ntask;
-  for (uint32_t t = 0; t < ntask; ++t) y.rq[at + t] = make_uint4(p, u, v, t);
+  return min(y.deg[u], y.deg[v]);
 }
 
 // Mode 0: warp per row, every live edge; S < k-2 is removed (truss.cpp:31).
@@ -1320,16 +1299,15 @@ k_mark(Graph g, Sym y) {
     const uint32_t base = g.row_ptr[u];
     for (uint32_t off = 0; off < d; off += 32) {
       const uint32_t idx = off + lane;
-      uint32_t ntask = 0, v = 0;
       const uint32_t p = base + idx;
       bool rm = false;
       if (idx < d) {
-        v = g.col[p];
-        const uint32_t sv = S[p];
+        const uint32_t v = g.col[p];
+        const uint32_t sv = u < h0 ? 0u : S[p];  // rows below h0 go whatever their count
         sum_s += sv;
         if (sv < thr || u < h0) {
           rm = true;
-          dcost += mark_removed(g, y, p, u, v, g.payload[p], &ntask);
+          dcost += mark_removed(g, y, p, u, v, g.payload[p]);
         } else {
           kcost += min(y.deg[u], y.deg[v]);
         }
@@ -1340,7 +1318,6 @@ k_mark(Graph g, Sym y) {
         y.sdirty[u] = 1;
         removed += __popc(rmask);
       }
-      push_tasks(g, y, ntask, p, u, v);
     }
   }
 #pragma unroll
@@ -1367,20 +1344,13 @@ k_mark_frontier(Graph g, Sym y) {
   const uint32_t* __restrict__ fq = par ? y.fq1 : y.fq0;
   const int lane = threadIdx.x & 31;
   unsigned long long dcost = 0;
-  const uint32_t stride = gridDim.x * blockDim.x;
-  const uint32_t n_round = (nf + stride - 1) / stride * stride;  // whole warps in every iteration
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n_round; i += stride) {
-    uint32_t ntask = 0, p = 0, u = 0, v = 0;
-    if (i < nf) {
-      const uint32_t id = fq[i];
-      p = y.pos_of[id];
-      u = y.erow[id];
-      v = g.col[p];
-      dcost += mark_removed(g, y, p, u, v, id, &ntask);
-      y.rdirty[u] = 1;
-      y.sdirty[u] = 1;
-    }
-    push_tasks(g, y, ntask, p, u, v);
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < nf; i += gridDim.x * blockDim.x) {
+    const uint32_t id = fq[i];
+    const uint32_t p = y.pos_of[id];
+    const uint32_t u = y.erow[id];
+    dcost += mark_removed(g, y, p, u, g.col[p], id);
+    y.rdirty[u] = 1;
+    y.sdirty[u] = 1;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) dcost += __shfl_xor_sync(0xffffffffu, dcost, o);
@@ -1468,11 +1438,45 @@ __device__ __forceinline__ void drop_support(const Graph& g, const Sym& y, uint3
   if (old == thr) append_coalesced(cnt_next, fq_next, id);
 }
 
-// Warp per delta task {slot, u, v, piece}: the removed edge e = (u, v) and a
-// kDeltaPiece window of the shorter of the two symmetric rows; each element w
-// is binary-searched in the longer row. A common neighbour w closes the
-// triangle {e, (u,w), (v,w)} of G_r. It is handled by its removed edge with
-// the smallest id (so once), and each surviving edge of it loses 1.
+// Triangles of G_r through the removed edge e = (u, v) at working slot p:
+// each element w of elements [lo, hi) of the shorter symmetric row is
+// binary-searched in the longer one (warp-cooperative, lanes over elements).
+// A common neighbour w closes {e, (u,w), (v,w)}; the triangle is handled by
+// its removed edge with the smallest id (so once), and each surviving edge
+// of it loses 1.
+__device__ __forceinline__ void delta_edge(const Graph& g, const Sym& y, uint32_t* __restrict__ S,
+                                           uint32_t* __restrict__ fq_next, uint32_t* cnt_next, uint32_t thr,
+                                           uint32_t p, uint32_t u, uint32_t v, uint32_t lo, uint32_t hi) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t e = g.payload[p];
+  const uint32_t du = y.deg[u], dv = y.deg[v];
+  const bool su = du <= dv;
+  const uint32_t la = su ? du : dv, lb = su ? dv : du;
+  const unsigned long long oa = y.ptr[su ? u : v], ob = y.ptr[su ? v : u];
+  const uint32_t* __restrict__ A = y.nbr + oa;
+  const uint32_t* __restrict__ B = y.nbr + ob;
+  hi = min(hi, la);
+  const uint32_t bmin = B[0], bmax = B[lb - 1];
+  for (uint32_t i = lo + lane; i < hi; i += 32) {
+    const uint32_t w = A[i];
+    if (w < bmin || w > bmax) continue;
+    const uint32_t j = lb_run(B, lb, w);
+    if (j < lb && B[j] == w) {
+      const uint32_t ea = y.eid[oa + i], eb = y.eid[ob + j];
+      const bool da = y.dead[ea], db = y.dead[eb];
+      if ((da && ea < e) || (db && eb < e)) continue;
+      if (!da) drop_support(g, y, S, fq_next, cnt_next, thr, ea);
+      if (!db) drop_support(g, y, S, fq_next, cnt_next, thr, eb);
+    }
+  }
+}
+
+constexpr uint32_t kDeltaInline = kDeltaPiece;  // longer intersections are queued as pieces
+
+// Warp per removed edge: after a full mark, rows are scanned for marked
+// slots; after a carried round, the frontier list is the removal set.
+// Intersections up to kDeltaInline elements run inline; longer ones are
+// queued as kDeltaPiece pieces {slot, u, v, piece} for k_delta_big.
 __global__ void __launch_bounds__(kPruneThreads)
 k_delta(Graph g, Sym y) {
   if (!g.st->carry) return;
@@ -1484,30 +1488,59 @@ k_delta(Graph g, Sym y) {
   const uint32_t par = g.st->fpar ^ 1u;  // next round's frontier
   uint32_t* __restrict__ fq_next = par ? y.fq1 : y.fq0;
   uint32_t* cnt_next = &g.st->nfq[par];
+  auto edge = [&](uint32_t p, uint32_t u, uint32_t v) {
+    const uint32_t mn = min(y.deg[u], y.deg[v]);
+    if (mn <= kDeltaInline) {
+      delta_edge(g, y, S, fq_next, cnt_next, thr, p, u, v, 0, mn);
+    } else if (lane == 0) {
+      const uint32_t np = (mn + kDeltaPiece - 1) / kDeltaPiece;
+      const uint32_t at = atomicAdd(&g.st->nrq, np);
+      for (uint32_t t = 0; t < np; ++t) y.rq[at + t] = make_uint4(p, u, v, t);
+    }
+  };
+  if (g.st->mode == 0) {
+    for (uint32_t u = warp + 1; u <= g.n; u += nwarps) {
+      const uint32_t d = g.deg[u];
+      if (d == 0) continue;
+      const uint32_t base = g.row_ptr[u];
+      for (uint32_t off = 0; off < d; off += 32) {
+        const uint32_t c = off + lane < d ? g.col[base + off + lane] : 0u;
+        unsigned m = __ballot_sync(0xffffffffu, c & kDeadMark);
+        while (m) {
+          const int b = __ffs(m) - 1;
+          m &= m - 1;
+          const uint32_t v = __shfl_sync(0xffffffffu, c, b) & ~kDeadMark;
+          edge(base + off + b, u, v);
+        }
+      }
+    }
+  } else {
+    const uint32_t fpar = g.st->fpar;
+    const uint32_t nf = g.st->nfq[fpar];
+    const uint32_t* __restrict__ fq = fpar ? y.fq1 : y.fq0;
+    for (uint32_t i = warp; i < nf; i += nwarps) {
+      const uint32_t id = fq[i];
+      const uint32_t p = y.pos_of[id];
+      edge(p, y.erow[id], g.col[p] & ~kDeadMark);
+    }
+  }
+}
+
+// Warp per queued piece of a long intersection.
+__global__ void __launch_bounds__(kPruneThreads)
+k_delta_big(Graph g, Sym y) {
+  if (!g.st->carry) return;
+  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  uint32_t* __restrict__ S = cur_S(g);
+  const uint32_t thr = g.st->threshold;
+  const uint32_t par = g.st->fpar ^ 1u;
+  uint32_t* __restrict__ fq_next = par ? y.fq1 : y.fq0;
+  uint32_t* cnt_next = &g.st->nfq[par];
   const uint32_t ntask = g.st->nrq;
   for (uint32_t t = warp; t < ntask; t += nwarps) {
     const uint4 q = y.rq[t];
-    const uint32_t e = g.payload[q.x];
-    const uint32_t du = y.deg[q.y], dv = y.deg[q.z];
-    const bool su = du <= dv;
-    const uint32_t la = su ? du : dv, lb = su ? dv : du;
-    const unsigned long long oa = y.ptr[su ? q.y : q.z], ob = y.ptr[su ? q.z : q.y];
-    const uint32_t* __restrict__ A = y.nbr + oa;
-    const uint32_t* __restrict__ B = y.nbr + ob;
-    const uint32_t lo = q.w * kDeltaPiece, hi = min(lo + kDeltaPiece, la);
-    const uint32_t bmin = B[0], bmax = B[lb - 1];
-    for (uint32_t i = lo + lane; i < hi; i += 32) {
-      const uint32_t w = A[i];
-      if (w < bmin || w > bmax) continue;
-      const uint32_t j = lb_run(B, lb, w);
-      if (j < lb && B[j] == w) {
-        const uint32_t ea = y.eid[oa + i], eb = y.eid[ob + j];
-        const bool da = y.dead[ea], db = y.dead[eb];
-        if ((da && ea < e) || (db && eb < e)) continue;
-        if (!da) drop_support(g, y, S, fq_next, cnt_next, thr, ea);
-        if (!db) drop_support(g, y, S, fq_next, cnt_next, thr, eb);
-      }
-    }
+    delta_edge(g, y, S, fq_next, cnt_next, thr, q.x, q.y, q.z, q.w * kDeltaPiece, (q.w + 1) * kDeltaPiece);
   }
 }
 
@@ -2108,14 +2141,20 @@ __global__ void k_work_din(Graph g, uint32_t* __restrict__ din) {
 }
 
 __global__ void k_work_L(Graph g, const uint32_t* __restrict__ din, unsigned long long* out) {
-  unsigned long long L = 0;
+  unsigned long long L = 0, Lt = 0;  // L, and its a12-tail part sum_v d+(d+-1)/2
   for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x + 1; v <= g.n; v += gridDim.x * blockDim.x) {
     const unsigned long long d = g.deg[v];
-    L += d * (d ? d - 1 : 0) / 2 + d * din[v];
+    const unsigned long long t = d * (d ? d - 1 : 0) / 2;
+    L += t + d * din[v];
+    Lt += t;
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) L += __shfl_xor_sync(0xffffffffu, L, o);
+  for (int o = 16; o > 0; o >>= 1) {
+    L += __shfl_xor_sync(0xffffffffu, L, o);
+    Lt += __shfl_xor_sync(0xffffffffu, Lt, o);
+  }
   if ((threadIdx.x & 31) == 0 && L) atomicAdd(out, L);
+  if ((threadIdx.x & 31) == 0 && Lt) atomicAdd(out + 1, Lt);
 }
 
 // ---------------------------------------------------------------------------
