@@ -1273,11 +1273,13 @@ __device__ __forceinline__ void append_coalesced(uint32_t* cnt, uint32_t* q, uin
 // far endpoint's symmetric row flagged (the caller flags row u). Flags are
 // plain byte stores (every writer stores 1); k_queues turns them into the
 // compaction queues. Returns min(du, dv) (the edge's delta cost).
+template <bool READ_FIRST>
 __device__ __forceinline__ uint32_t mark_removed(const Graph& g, const Sym& y, uint32_t p, uint32_t u, uint32_t v,
                                                  uint32_t id) {
   g.col[p] = v | kDeadMark;
   y.dead[id] = 1;
-  y.sdirty[v] = 1;
+  // full marks flag hubs from many rows at once: read first, store once
+  if (!READ_FIRST || !y.sdirty[v]) y.sdirty[v] = 1;
   return min(y.deg[u], y.deg[v]);
 }
 
@@ -1307,7 +1309,7 @@ k_mark(Graph g, Sym y) {
         sum_s += sv;
         if (sv < thr || u < h0) {
           rm = true;
-          dcost += mark_removed(g, y, p, u, v, g.payload[p]);
+          dcost += mark_removed<true>(g, y, p, u, v, g.payload[p]);
         } else {
           kcost += min(y.deg[u], y.deg[v]);
         }
@@ -1348,7 +1350,7 @@ k_mark_frontier(Graph g, Sym y) {
     const uint32_t id = fq[i];
     const uint32_t p = y.pos_of[id];
     const uint32_t u = y.erow[id];
-    dcost += mark_removed(g, y, p, u, g.col[p], id);
+    dcost += mark_removed<false>(g, y, p, u, g.col[p], id);
     y.rdirty[u] = 1;
     y.sdirty[u] = 1;
   }

@@ -13,13 +13,14 @@ fix = -1; rnd = None; rounds = []
 for k, us in out:
     if k == "k_begin":
         fix += 1
-    if k == "k_plan_count" and fix >= 0:
+    if k in ("k_plan_count", "k_support_a22") and fix >= 0 and (rnd is None or "k_control_inc" in rnd or "k_control" in rnd):
         rnd = collections.OrderedDict(); rounds.append((fix, rnd))
     if rnd is not None:
         rnd[k] = rnd.get(k, 0) + us
-keys = ["k_support_chunked", "k_mark", "k_mark_frontier", "k_queues", "k_delta", "k_inc_rows<0>", "k_inc_rows<1>",
-        "k_inc_sym<0>", "k_inc_sym<1>", "k_inc_zero", "k_publish_inc<0>", "k_publish_inc<1>", "k_scatter_live"]
-short = ["sup", "mark", "mfr", "q", "delta", "rows", "rowsH", "sym", "symH", "zero", "pub", "pubH", "scat"]
+keys = ["k_support_a22", "k_support_chunked", "k_mark", "k_mark_frontier", "k_queues", "k_delta", "k_delta_big",
+        "k_inc_rows<0>", "k_inc_rows<1>", "k_inc_sym<0>", "k_inc_sym<1>", "k_inc_zero", "k_publish_inc<0>",
+        "k_publish_inc<1>"]
+short = ["a22", "chunk", "mark", "mfr", "q", "delta", "dbig", "rows", "rowsH", "sym", "symH", "zero", "pub", "pubH"]
 print("fx rd " + " ".join(f"{s:>7s}" for s in short) + "   total")
 for i, (f, r) in enumerate(rounds):
     tot = sum(r.values())
