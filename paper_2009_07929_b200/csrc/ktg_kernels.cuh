@@ -713,6 +713,7 @@ k_support_chunked(Graph g) {
 // slot (i, c) once. Tasks are (chunk, batch of kA22Batch pivots), static.
 constexpr int kA22Batch = 256;
 constexpr int kA22TableBits = 11;          // 2048 slots for <= 512 entries (load <= 0.25)
+constexpr int kA22Strip = 256;             // flat tail elements a warp takes per grab
 constexpr int kA22Table = 1 << kA22TableBits;
 
 struct A22 {
@@ -883,10 +884,10 @@ k_support_a22(Graph g, Sym y, A22 a) {
     // 4. flattened tail elements, strips grabbed dynamically by warps
     for (;;) {
       uint32_t base = 0;
-      if (lane == 0) base = atomicAdd(&s.next, (uint32_t)kStrip);
+      if (lane == 0) base = atomicAdd(&s.next, (uint32_t)kA22Strip);
       base = __shfl_sync(0xffffffffu, base, 0);
       if (base >= W) break;
-      const uint32_t lim = min(base + (uint32_t)kStrip, W);
+      const uint32_t lim = min(base + (uint32_t)kA22Strip, W);
       uint32_t p;
       {
         uint32_t lo = 0, hi = kA22Batch;
