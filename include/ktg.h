@@ -192,6 +192,10 @@ typedef struct {
                            supports were carried from the previous round */
   uint32_t pad;
   uint64_t L_tail;      /* the a12-tail part of L: sum_v d+(d+-1)/2       */
+  uint64_t delta_cost;  /* carried runs: sum of min(du, dv) over removals  */
+  uint64_t keep_cost;   /* carried runs: the same over the survivors       */
+  uint32_t delta_pieces;/* carried runs: long intersections queued         */
+  uint32_t carried;     /* carried runs: 1 if the round carried its S      */
 } ktg_round_work;
 
 ktg_status ktg_engine_create(const ktg_options* opt, ktg_engine** out);

@@ -957,6 +957,10 @@ ktg_status run_loop(ktg_engine* e, bool want_sync) {
     if (recording) {
       w.triangles = e->h_st->last_triangles;
       w.removed = removed;
+      w.delta_cost = e->h_st->last_dcost;
+      w.keep_cost = e->h_st->last_kcost;
+      w.delta_pieces = e->h_st->last_nrq;
+      w.carried = e->h_st->last_carry;
       if (timing) {
         float ms = 0;
         KTG_CUDA(cudaEventElapsedTime(&ms, e->evs0, e->evs1));

@@ -62,6 +62,10 @@ struct DevState {
   unsigned int nheavy_sym;           // long symmetric rows queued for CTA compaction
   unsigned int h0;                   // round 0 from pristine: first rank of degree >= k-1 (0: off)
   unsigned int pristine;             // this round runs on the pristine working layout
+  unsigned int last_nrq;             // statistics of the last completed round:
+  unsigned int last_carry;           //   queued delta pieces, whether it carried,
+  unsigned long long last_dcost;     //   its delta cost and keep cost
+  unsigned long long last_kcost;
 };
 
 struct Graph {
@@ -1829,6 +1833,10 @@ __global__ void k_control_inc(DevState* st, unsigned long long* hist, cudaGraphC
   st->live -= removed;
   if (st->mode == 0) st->last_triangles = st->sum_s / 3;
   st->live_cost = st->keep_cost;
+  st->last_nrq = st->nrq;
+  st->last_carry = st->carry;
+  st->last_dcost = st->delta_cost;
+  st->last_kcost = st->keep_cost;
   st->mode = st->carry;
   st->h0 = 0;  // round 0 only
   st->pristine = 0;

@@ -151,7 +151,8 @@ class _RunInfo(ctypes.Structure):
 class _RoundWork(ctypes.Structure):
     _fields_ = [("live_edges", _u64), ("L", _u64), ("triangles", _u64), ("removed", _u64),
                 ("support_ms", ctypes.c_double), ("full_pass", ctypes.c_uint32), ("pad", ctypes.c_uint32),
-                ("L_tail", _u64)]
+                ("L_tail", _u64), ("delta_cost", _u64), ("keep_cost", _u64),
+                ("delta_pieces", ctypes.c_uint32), ("carried", ctypes.c_uint32)]
 
 
 FLAG_HOST_LOOP = 1
