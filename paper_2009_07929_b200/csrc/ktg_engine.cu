@@ -183,7 +183,7 @@ struct ktg_engine {
   bool sym_ready = false;
   bool inc_active = false;    // the current fixpoint carries supports
   bool pristine = false;      // the working layout holds the pristine graph (after load / reset)
-  uint32_t delta_ratio16 = 1;  // carry when delta_cost <= keep_cost / 16 (s20 sweep calibration, scripts/ratio_scan.py)
+  double delta_ratio = 0.0625;  // carry when delta_cost <= ratio * keep_cost (s20 sweep calibration, scripts/ratio_scan.py)
 
   unsigned long long* d_workL = nullptr;
   DevState* d_st = nullptr;
@@ -310,7 +310,7 @@ ktg_status engine_init(const ktg_options* opt, ktg_engine* e) {
                                        " is not sm_100 (this build targets sm_100a only)");
   e->num_sms = prop.multiProcessorCount;
   if (const char* r = getenv("KTG_SCAN_RATIO")) e->scan_ratio = (uint32_t)std::max(1, atoi(r));
-  if (const char* r = getenv("KTG_DELTA_RATIO")) e->delta_ratio16 = (uint32_t)std::max(0.0, 16.0 * atof(r));
+  if (const char* r = getenv("KTG_DELTA_RATIO")) e->delta_ratio = std::max(0.0, atof(r));
   if (e->opt.stream) {
     e->stream = static_cast<cudaStream_t>(e->opt.stream);
   } else {
@@ -876,7 +876,7 @@ ktg_status begin_run(ktg_engine* e, uint32_t k, int parity) {
     parity = 0;
   }
   k_begin<<<1, 1, 0, e->stream>>>(e->d_st, k >= 2 ? k - 2 : 0, e->opt.width_bits == 16 ? 1 : 0, parity,
-                                  e->inc_active ? 1u : 0u, e->delta_ratio16);
+                                  e->inc_active ? 1u : 0u, e->delta_ratio);
   if (e->inc_active && e->pristine) {
     if (!flag(e, KTG_FLAG_NO_DEGREE_BOUND))
       k_heavy_rank<<<1, 1, 0, e->stream>>>(e->d_st, e->sym_deg_p.p, e->wl.n);
@@ -1020,7 +1020,7 @@ ktg_status support_pass(ktg_engine* e, int parity, uint64_t* triangles, bool max
   Layout& L = e->act();
   Graph g = e->graph_of(L);
   e->inc_active = false;
-  k_begin<<<1, 1, 0, e->stream>>>(e->d_st, 0, e->opt.width_bits == 16 ? 1 : 0, parity, 0u, e->delta_ratio16);
+  k_begin<<<1, 1, 0, e->stream>>>(e->d_st, 0, e->opt.width_bits == 16 ? 1 : 0, parity, 0u, e->delta_ratio);
   k_plan_count<<<(L.nchunks + 255) / 256, 256, 0, e->stream>>>(g, 0);
   k_plan_write<<<1, 1024, 0, e->stream>>>(g);
   if (flag(e, KTG_FLAG_NAIVE_SUPPORT))

@@ -49,8 +49,9 @@ struct DevState {
   unsigned int inc;                  // 1: supports are carried across rounds when cheaper
   unsigned int mode;                 // this round: 0 = recompute supports, 1 = carried (delta)
   unsigned int nrq;                  // delta tasks queued by k_mark this round
-  unsigned int delta_ratio16;        // carry when 16 * delta_cost <= ratio16 * keep_cost
+  unsigned int pad3;
   unsigned int pad2;
+  double delta_ratio;                // carry when delta_cost <= delta_ratio * keep_cost
   unsigned long long sum_s;          // sum of S over live edges (k_mark): 3 * triangles
   unsigned long long delta_cost;     // sum over removed edges of min(du, dv)
   unsigned long long keep_cost;      // sum over surviving edges of min(du, dv)
@@ -1420,7 +1421,7 @@ __global__ void k_set_pristine(DevState* st) { st->pristine = 1; }
 __global__ void k_decide(DevState* st) {
   if (st->mode == 1) st->keep_cost = st->live_cost > st->delta_cost ? st->live_cost - st->delta_cost : 0;
   st->carry = (st->inc && st->removed != 0 &&
-               16ull * st->delta_cost <= (unsigned long long)st->delta_ratio16 * st->keep_cost)
+               (double)st->delta_cost <= st->delta_ratio * (double)st->keep_cost)
                   ? 1u
                   : 0u;
 }
@@ -2089,7 +2090,7 @@ __global__ void k_scatter_live(Graph w, const uint32_t* __restrict__ col_pristin
 // Loop control
 // ---------------------------------------------------------------------------
 __global__ void k_begin(DevState* st, uint32_t threshold, uint32_t width16, int parity, uint32_t inc,
-                        uint32_t delta_ratio16) {
+                        double delta_ratio) {
   st->inc = inc;
   st->mode = 0;
   st->nrq = 0;
@@ -2101,7 +2102,7 @@ __global__ void k_begin(DevState* st, uint32_t threshold, uint32_t width16, int 
   st->h0 = 0;
   st->pristine = 0;
   st->live_cost = 0;
-  st->delta_ratio16 = delta_ratio16;
+  st->delta_ratio = delta_ratio;
   st->sum_s = 0;
   st->delta_cost = 0;
   st->keep_cost = 0;
