@@ -31,6 +31,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <chrono>
 #include <functional>
 #include <cstdio>
 #include <cstdlib>
@@ -475,14 +476,13 @@ ktg_status build_a22(ktg_engine* e) {
   const uint32_t Q = W.nchunks;
   const cudaStream_t s = e->stream;
   e->a22_ready = false;
-  KTG_TRY(e->a22_pe.ensure(m));
   KTG_TRY(e->a22_pin.ensure(m));
   KTG_TRY(e->a22_off.ensure(nb));
   KTG_TRY(e->a22_jfirst.ensure(Q));
   KTG_TRY(e->a22_cnt.ensure((size_t)Q + 1));
   Sym y = e->sym();
-  k_a22_pe<<<e->prune_grid, kPruneThreads, 0, s>>>(y, e->sym_sizes.p + 3 * nb, e->din.p, n, e->a22_pe.p,
-                                                   e->a22_off.p);
+  // a22_pe (the sorted in-list ids) was written by k_sym_fill_in
+  k_u64_to_u32<<<4 * e->num_sms, 256, 0, s>>>(e->sym_sizes.p + 3 * nb, (uint32_t)nb, e->a22_off.p);
   k_a22_pin<<<4 * e->num_sms, 256, 0, s>>>(e->a22_pe.p, m, y, e->a22_pin.p);
   k_chunk_first<<<(Q + 255) / 256, 256, 0, s>>>(W.row_ptr.p, n, W.slots, Q, e->a22_jfirst.p);
   k_a22_count<<<(Q + 256) / 256, 256, 0, s>>>(e->a22_jfirst.p, W.chunk_row.p, e->a22_off.p, Q, e->a22_cnt.p);
@@ -550,8 +550,10 @@ ktg_status build_sym(ktg_engine* e) {
   KTG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, sz, e->sym_ptr.p, (int)nb, s));
   uint32_t B = 1;
   while ((1ull << B) <= n) ++B;
-  KTG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp2, e->keys.p, e->keys_sorted.p, e->vals.p,
-                                           e->vals_sorted.p, (int64_t)m, 0, 2 * B, s));
+  // in-lists: a STABLE sort of the working edges (emitted in (u, v) order)
+  // by v alone keeps every in-list ascending in u -- B key bits, not 2B
+  KTG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp2, e->vals.p, e->vals_sorted.p, e->keys.p,
+                                           e->keys_sorted.p, (int64_t)m, 0, (int)B, s));
   KTG_TRY(e->cub_tmp.ensure(std::max(tmp, tmp2)));
   // tot = din + dout (one add kernel via the scan of the two halves)
   k_add_u64<<<4 * e->num_sms, 256, 0, s>>>(sz + nb, sz + 2 * nb, (uint32_t)nb, sz);
@@ -561,14 +563,16 @@ ktg_status build_sym(ktg_engine* e) {
   KTG_CUDA(cub::DeviceScan::ExclusiveSum(e->cub_tmp.p, tmp, sz + nb, sz + 3 * nb, (int)nb, s));
   tmp = e->cub_tmp.cap;
   KTG_CUDA(cub::DeviceScan::ExclusiveSum(e->cub_tmp.p, tmp, sz + 2 * nb, sz + 4 * nb, (int)nb, s));
-  k_sym_in_keys<<<e->prune_grid, kPruneThreads, 0, s>>>(g, B, e->keys.p, e->vals.p, sz + 4 * nb);
+  k_sym_in_keys<<<e->prune_grid, kPruneThreads, 0, s>>>(g, e->vals.p, e->keys.p, sz + 4 * nb);
   KTG_CUDA(cudaGetLastError());
   tmp = e->cub_tmp.cap;
-  KTG_CUDA(cub::DeviceRadixSort::SortPairs(e->cub_tmp.p, tmp, e->keys.p, e->keys_sorted.p, e->vals.p,
-                                           e->vals_sorted.p, (int64_t)m, 0, 2 * B, s));
+  KTG_CUDA(cub::DeviceRadixSort::SortPairs(e->cub_tmp.p, tmp, e->vals.p, e->vals_sorted.p, e->keys.p,
+                                           e->keys_sorted.p, (int64_t)m, 0, (int)B, s));
   Sym y = e->sym();
-  k_sym_fill<<<e->prune_grid, kPruneThreads, 0, s>>>(g, B, e->keys_sorted.p, e->vals_sorted.p, sz + 3 * nb,
-                                                     e->din.p, y);
+  KTG_TRY(e->a22_pe.ensure(m));
+  k_sym_fill_in<<<8 * e->num_sms, 256, 0, s>>>(e->vals_sorted.p, e->keys_sorted.p, m, sz + 3 * nb, y,
+                                               e->a22_pe.p);
+  k_sym_fill_out<<<e->prune_grid, kPruneThreads, 0, s>>>(g, e->din.p, y);
   KTG_CUDA(cudaMemsetAsync(e->d_workL, 0, 8, s));
   k_sym_pos<<<e->prune_grid, kPruneThreads, 0, s>>>(g, y, e->d_workL);
   KTG_CUDA(cudaGetLastError());
@@ -610,13 +614,29 @@ ktg_status engine_load(ktg_engine* e, const uint32_t* row_ptr, uint32_t n, const
   e->caller_stale = false;
   KTG_TRY(C.row_ptr.ensure((size_t)n + 2));
   KTG_TRY(C.col.ensure(slots + 4));
+  // KTG_LOAD_TIMING=1: per-phase wall times of the load on stderr (debug)
+  static const bool timing = getenv("KTG_LOAD_TIMING") != nullptr;
+  std::vector<std::pair<const char*, double>> marks;
+  auto mark = [&](const char* what) {
+    if (!timing) return;
+    cudaStreamSynchronize(e->stream);
+    marks.emplace_back(what, std::chrono::duration<double, std::milli>(
+                                 std::chrono::steady_clock::now().time_since_epoch()).count());
+  };
+  mark("start");
   if (row_ptr) KTG_CUDA(cudaMemcpyAsync(C.row_ptr.p, row_ptr, ((size_t)n + 2) * 4, kind, e->stream));
   if (col) KTG_CUDA(cudaMemcpyAsync(C.col.p, col, slots * 4, kind, e->stream));
+  mark("upload");
   KTG_TRY(prepare_layout(e, C, keep_pristine || e->reoriented));
+  mark("caller layout");
   if (e->reoriented) {
     KTG_TRY(build_working(e));
+    mark("working layout");
     if (!flag(e, KTG_FLAG_RECOMPUTE)) KTG_TRY(build_sym(e));
+    mark("symmetric rows + A22 plan");
   }
+  for (size_t i = 1; i < marks.size(); ++i)
+    fprintf(stderr, "ktg load: %-26s %8.3f ms\n", marks[i].first, marks[i].second - marks[i - 1].second);
   return KTG_OK;
 }
 

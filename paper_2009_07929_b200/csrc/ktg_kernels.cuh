@@ -996,20 +996,6 @@ __global__ void k_a22_fill(const uint32_t* __restrict__ cnt_off, uint32_t nchunk
   for (uint32_t b = 0; b < c; ++b) tasks[o + b] = make_uint2(q, b);
 }
 
-// Load time: the in-part of every pristine symmetric row (edge ids), packed.
-__global__ void k_a22_pe(Sym y, const unsigned long long* __restrict__ inoff, const uint32_t* __restrict__ din,
-                         uint32_t n, uint32_t* __restrict__ pe, uint32_t* __restrict__ pin_off) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t v = warp; v <= n + 1; v += nwarps) {
-    const unsigned long long o = inoff[v], b = y.ptr[v];
-    if (lane == 0) pin_off[v] = (uint32_t)o;
-    if (v == 0 || v > n) continue;
-    for (uint32_t x = lane; x < din[v]; x += 32) pe[o + x] = y.eid[b + x];
-  }
-}
-
 // Paper Listing 1 / support.cpp:115-127 as written: one thread per slot,
 // sequential two-pointer merge. Cross-check kernel only.
 __global__ void k_support_naive(Graph g) {
@@ -1879,11 +1865,11 @@ __global__ void k_inc_triangles_done(DevState* st) {
   st->sum_s = 0;
 }
 
-// Symmetric adjacency build (load time). In-neighbour keys (v << B | u) for
-// every live working edge u -> v, with the edge id as value; sorted, they
-// give each row's in-part in ascending order.
-__global__ void k_sym_in_keys(Graph w, uint32_t B, unsigned long long* __restrict__ keys,
-                              uint32_t* __restrict__ vals, const unsigned long long* __restrict__ offs) {
+// Symmetric adjacency build (load time). For every live working edge u -> v
+// (emitted in working (u, v) order): key v, value u << 32 | id. A stable sort
+// by v leaves each in-list ascending in u.
+__global__ void k_sym_in_keys(Graph w, uint32_t* __restrict__ keys, unsigned long long* __restrict__ vals,
+                              const unsigned long long* __restrict__ offs) {
   const int lane = threadIdx.x & 31;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
@@ -1891,33 +1877,42 @@ __global__ void k_sym_in_keys(Graph w, uint32_t B, unsigned long long* __restric
     const uint32_t d = w.deg[u], base = w.row_ptr[u];
     const unsigned long long o = offs[u];
     for (uint32_t x = lane; x < d; x += 32) {
-      keys[o + x] = ((unsigned long long)w.col[base + x] << B) | u;
-      vals[o + x] = w.payload[base + x];
+      keys[o + x] = w.col[base + x];
+      vals[o + x] = ((unsigned long long)u << 32) | w.payload[base + x];
     }
   }
 }
 
-// Row v of the symmetric adjacency = sorted in-part (indices [inoff[v],
-// inoff[v]+din[v]) of the sorted keys) followed by the out-part (working row v).
-__global__ void k_sym_fill(Graph w, uint32_t B, const unsigned long long* __restrict__ keys,
-                           const uint32_t* __restrict__ vals, const unsigned long long* __restrict__ inoff,
-                           const uint32_t* __restrict__ din, Sym y) {
+// Element-parallel: sorted entry i of the in-lists goes to position
+// i - inoff[v] of symmetric row v (its in-part); its id is also the i-th
+// entry of the A22 in-edge list.
+__global__ void k_sym_fill_in(const uint32_t* __restrict__ vkeys, const unsigned long long* __restrict__ vals,
+                              uint64_t m, const unsigned long long* __restrict__ inoff, Sym y,
+                              uint32_t* __restrict__ pe) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t v = vkeys[i];
+    const unsigned long long pv = vals[i];
+    const unsigned long long dst = y.ptr[v] + (i - inoff[v]);
+    y.nbr[dst] = (uint32_t)(pv >> 32);
+    y.eid[dst] = (uint32_t)pv;
+    pe[i] = (uint32_t)pv;
+  }
+}
+
+// Out-part of symmetric row v = working row v (warp per row; working rows
+// are short in degree order); live length = in + out.
+__global__ void k_sym_fill_out(Graph w, const uint32_t* __restrict__ din, Sym y) {
   const int lane = threadIdx.x & 31;
   const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
   const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-  const unsigned long long mask = (1ull << B) - 1;
   for (uint32_t v = warp + 1; v <= w.n; v += nwarps) {
-    const unsigned long long dst = y.ptr[v], io = inoff[v];
-    const uint32_t di = din[v], d = w.deg[v], base = w.row_ptr[v];
-    for (uint32_t x = lane; x < di; x += 32) {
-      y.nbr[dst + x] = (uint32_t)(keys[io + x] & mask);
-      y.eid[dst + x] = vals[io + x];
-    }
+    const unsigned long long dst = y.ptr[v] + din[v];
+    const uint32_t d = w.deg[v], base = w.row_ptr[v];
     for (uint32_t x = lane; x < d; x += 32) {
-      y.nbr[dst + di + x] = w.col[base + x];
-      y.eid[dst + di + x] = w.payload[base + x];
+      y.nbr[dst + x] = w.col[base + x];
+      y.eid[dst + x] = w.payload[base + x];
     }
-    if (lane == 0) y.deg[v] = di + d;
+    if (lane == 0) y.deg[v] = din[v] + d;
   }
 }
 
@@ -1946,6 +1941,10 @@ __global__ void k_sym_pos(Graph w, Sym y, unsigned long long* __restrict__ cap) 
 __global__ void k_add_u64(const unsigned long long* __restrict__ a, const unsigned long long* __restrict__ b,
                           uint32_t n, unsigned long long* __restrict__ c) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) c[i] = a[i] + b[i];
+}
+
+__global__ void k_u64_to_u32(const unsigned long long* __restrict__ a, uint32_t n, uint32_t* __restrict__ b) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) b[i] = (uint32_t)a[i];
 }
 
 __global__ void k_u32_to_u64(const uint32_t* __restrict__ a, uint32_t n, unsigned long long* __restrict__ b) {
@@ -2026,24 +2025,28 @@ __global__ void k_rank_assign(const unsigned long long* __restrict__ sorted, uin
     rank[(uint32_t)sorted[i]] = i + 1;
 }
 
-// Edge keys (a << B | b, a < b ranks) with the caller slot as value; warp per
-// caller row; offs = exclusive prefix of the caller live degrees.
+// Edge keys (a << B | b, a < b ranks) with the caller slot as value,
+// slot-parallel (the row of a live slot by binary search over row_ptr);
+// offs = exclusive prefix of the caller live degrees.
 __global__ void k_edge_keys(Graph g, const uint32_t* __restrict__ rank, const uint32_t* __restrict__ offs,
                             uint32_t B, unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals,
                             uint32_t* __restrict__ cnt) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t u = warp + 1; u <= g.n; u += nwarps) {
-    const uint32_t d = g.deg[u], base = g.row_ptr[u], o = offs[u];
-    const uint32_t ru = rank[u];
-    for (uint32_t x = lane; x < d; x += 32) {
-      const uint32_t rv = rank[g.col[base + x]];
-      const uint32_t a = min(ru, rv), b = max(ru, rv);
-      keys[o + x] = ((unsigned long long)a << B) | b;
-      vals[o + x] = base + x;
-      atomicAdd(&cnt[a], 1u);
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < g.slots;
+       x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t c = g.col[x];
+    if (c == 0) continue;
+    uint32_t lo = 0, hi = g.n + 2;  // row = upper_bound(row_ptr, x) - 1
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (g.row_ptr[mid] <= (uint32_t)x) lo = mid + 1; else hi = mid;
     }
+    const uint32_t u = lo - 1;
+    const uint32_t o = offs[u] + ((uint32_t)x - g.row_ptr[u]);
+    const uint32_t ru = rank[u], rv = rank[c];
+    const uint32_t a = min(ru, rv), b = max(ru, rv);
+    keys[o] = ((unsigned long long)a << B) | b;
+    vals[o] = (uint32_t)x;
+    atomicAdd(&cnt[a], 1u);
   }
 }
 
@@ -2142,13 +2145,13 @@ __global__ void k_control(DevState* st, unsigned long long* hist, cudaGraphCondi
 // ---------------------------------------------------------------------------
 // Per-round closed-form work, optional
 // ---------------------------------------------------------------------------
+// Live in-degree: slot-parallel (a row's live slots are its nonzero ones;
+// label-order hub rows are too long for a warp per row).
 __global__ void k_work_din(Graph g, uint32_t* __restrict__ din) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t v = warp + 1; v <= g.n; v += nwarps) {
-    const uint32_t d = g.deg[v], base = g.row_ptr[v];
-    for (uint32_t x = lane; x < d; x += 32) atomicAdd(&din[g.col[base + x]], 1u);
+  for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < g.slots;
+       x += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t c = g.col[x];
+    if (c) atomicAdd(&din[c], 1u);
   }
 }
 
