@@ -720,6 +720,7 @@ constexpr int kA22Batch = 256;
 constexpr int kA22TableBits = 11;          // 2048 slots for <= 512 entries (load <= 0.25)
 constexpr int kA22Strip = 256;             // flat tail elements a warp takes per grab
 constexpr int kA22Table = 1 << kA22TableBits;
+constexpr int kA22FiltWords = 512;         // 16K filter bits for <= 512 entries (~3% false positives)
 
 struct A22 {
   const uint32_t* pe;        // in-edge ids, grouped by j (pristine in-lists)
@@ -733,7 +734,6 @@ struct A22 {
 struct A22Smem {
   uint32_t A[kChunk];
   uint32_t cntA[kChunk];
-  uint16_t nz[kChunk];
   uint32_t rte[kChunk + 2];          // per row of the chunk: run [tb, te) as tb << 16 | te, or ~0
   uint32_t roff[kChunk + 2];         // pin_off of the chunk's rows (+1)
   uint32_t ps[kA22Batch];            // pivot slot (i, j)
@@ -741,15 +741,20 @@ struct A22Smem {
   uint32_t prun[kA22Batch];          // j's run tb << 16 | te
   uint32_t cntP[kA22Batch];
   uint32_t pref[kA22Batch + 1];
+  uint32_t filt[kA22FiltWords];      // membership bits of (value, run end): most misses stop here
   uint2 tab[kA22Table];              // open addressing: {value (0 = empty), chunk position}
   uint32_t red[kSupportThreads / 32];
   uint32_t task;
   uint32_t next;
 };
 
-__device__ __forceinline__ uint32_t a22_hash(uint32_t v, uint32_t te) {
-  return ((v ^ (te * 0x85EBCA6Bu)) * 2654435761u) >> (32 - kA22TableBits);
+// One multiplicative hash of (value, run end): the table slot takes its top
+// kA22TableBits bits, the filter bit a fold of the rest.
+__device__ __forceinline__ uint32_t a22_mix(uint32_t v, uint32_t te) {
+  return (v ^ (te * 0x85EBCA6Bu)) * 2654435761u;
 }
+__device__ __forceinline__ uint32_t a22_slot(uint32_t h) { return h >> (32 - kA22TableBits); }
+__device__ __forceinline__ uint32_t a22_fbit(uint32_t h) { return (h ^ (h >> 15)) & (kA22FiltWords * 32 - 1); }
 
 __global__ void __launch_bounds__(kSupportThreads)
 k_support_a22(Graph g, Sym y, A22 a) {
@@ -848,6 +853,7 @@ k_support_a22(Graph g, Sym y, A22 a) {
 
     // 3. stage the chunk, next zeros, (value, run end) hash -- as k_support_chunked
     for (uint32_t b = tid; b < (uint32_t)kA22Table; b += kSupportThreads) s.tab[b] = make_uint2(0, 0);
+    for (uint32_t b = tid; b < (uint32_t)kA22FiltWords; b += kSupportThreads) s.filt[b] = 0;
     uint32_t first_zero = 0xffffffffu;
 #pragma unroll
     for (int e = 0; e < EPT; ++e) {
@@ -876,9 +882,11 @@ k_support_a22(Graph g, Sym y, A22 a) {
         const uint32_t x = tid * EPT + e;
         const uint32_t v = s.A[x];
         if (x < alen && v == 0) cur = x;
-        s.nz[x] = (uint16_t)min(cur, (uint32_t)kChunk);
         if (v != 0) {  // claim the first free slot from home (values are >= 1)
-          uint32_t h = a22_hash(v, cur);
+          const uint32_t hh = a22_mix(v, cur);
+          const uint32_t fb = a22_fbit(hh);
+          atomicOr(&s.filt[fb >> 5], 1u << (fb & 31));
+          uint32_t h = a22_slot(hh);
           while (atomicCAS(&s.tab[h].x, 0u, v) != 0u) h = (h + 1) & (kA22Table - 1);
           s.tab[h].y = x;
         }
@@ -887,20 +895,21 @@ k_support_a22(Graph g, Sym y, A22 a) {
     __syncthreads();
 
     // 4. flattened tail elements, strips grabbed dynamically by warps
+    uint32_t tri_task = 0;
     for (;;) {
       uint32_t base = 0;
       if (lane == 0) base = atomicAdd(&s.next, (uint32_t)kA22Strip);
       base = __shfl_sync(0xffffffffu, base, 0);
       if (base >= W) break;
       const uint32_t lim = min(base + (uint32_t)kA22Strip, W);
+      // pivot holding base: p = #{q in [1, kA22Batch) : pref[q] <= base}
+      // (pref ascends), two ballots over groups of 8 instead of a search
+      static_assert(kA22Batch == 256, "two-level ballot assumes 32 groups of 8");
       uint32_t p;
       {
-        uint32_t lo = 0, hi = kA22Batch;
-        while (lo < hi) {
-          const uint32_t mid = (lo + hi) >> 1;
-          if (s.pref[mid + 1] <= base) lo = mid + 1; else hi = mid;
-        }
-        p = lo;
+        const uint32_t g = __popc(__ballot_sync(0xffffffffu, lane < 31 && s.pref[8 * (lane + 1)] <= base));
+        const uint32_t c2 = __popc(__ballot_sync(0xffffffffu, lane < 7 && s.pref[8 * g + 1 + lane] <= base));
+        p = 8 * g + c2;
       }
       uint32_t pe_ = s.pref[p + 1], pb = s.pref[p], plo = s.plo[p], prun = s.prun[p];
       for (uint32_t f = base + lane; f < lim; f += 32) {
@@ -917,23 +926,28 @@ k_support_a22(Graph g, Sym y, A22 a) {
         const uint32_t c = col[slot];
         const uint32_t tb = prun >> 16, te = prun & 0xffffu;
         // (value, run) lookup: the value may also sit in other rows' runs
-        uint32_t x = kChunk;
-        for (uint32_t h = a22_hash(c, te);; h = (h + 1) & (kA22Table - 1)) {
-          const uint2 e = s.tab[h];
-          if (e.x == 0) break;
-          if (e.x == c && e.y >= tb && e.y < te) {
-            x = e.y;
-            break;
+        const uint32_t hh = a22_mix(c, te);
+        const uint32_t fb = a22_fbit(hh);
+        if (s.filt[fb >> 5] & (1u << (fb & 31))) {
+          uint32_t x = kChunk;
+          for (uint32_t h = a22_slot(hh);; h = (h + 1) & (kA22Table - 1)) {
+            const uint2 e = s.tab[h];
+            if (e.x == 0) break;
+            if (e.x == c && e.y - tb < te - tb) {
+              x = e.y;
+              break;
+            }
           }
-        }
-        if (x < (uint32_t)kChunk) {
-          atomicAdd(&s.cntA[x], 1u);
-          atomicAdd(&S[slot], 1u);
-          atomicAdd(&s.cntP[p], 1u);
-          ++tri_local;
+          if (x < (uint32_t)kChunk) {
+            atomicAdd(&s.cntA[x], 1u);
+            atomicAdd(&S[slot], 1u);
+            atomicAdd(&s.cntP[p], 1u);
+            ++tri_task;
+          }
         }
       }
     }
+    tri_local += tri_task;
     __syncthreads();
 
     // 5. flush shared counts (A22 slots, pivots)
