@@ -185,6 +185,7 @@ struct ktg_engine {
   bool inc_active = false;    // the current fixpoint carries supports
   bool pristine = false;      // the working layout holds the pristine graph (after load / reset)
   double delta_ratio = 0.0625;  // carry when delta_cost <= ratio * keep_cost (s20 sweep calibration, scripts/ratio_scan.py)
+  double delta_ratio0 = 0.0625; // the same for round 0 from the pristine graph
 
   unsigned long long* d_workL = nullptr;
   DevState* d_st = nullptr;
@@ -311,7 +312,8 @@ ktg_status engine_init(const ktg_options* opt, ktg_engine* e) {
                                        " is not sm_100 (this build targets sm_100a only)");
   e->num_sms = prop.multiProcessorCount;
   if (const char* r = getenv("KTG_SCAN_RATIO")) e->scan_ratio = (uint32_t)std::max(1, atoi(r));
-  if (const char* r = getenv("KTG_DELTA_RATIO")) e->delta_ratio = std::max(0.0, atof(r));
+  if (const char* r = getenv("KTG_DELTA_RATIO")) e->delta_ratio = e->delta_ratio0 = std::max(0.0, atof(r));
+  if (const char* r = getenv("KTG_DELTA_RATIO0")) e->delta_ratio0 = std::max(0.0, atof(r));
   if (e->opt.stream) {
     e->stream = static_cast<cudaStream_t>(e->opt.stream);
   } else {
@@ -340,8 +342,7 @@ ktg_status engine_init(const ktg_options* opt, ktg_engine* e) {
   KTG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_p, k_prune_light<0>, kPruneThreads, 0));
   e->prune_grid = std::max(1, per_sm_p) * e->num_sms;
   e->heavy_grid = 2 * e->num_sms;
-  e->a22_smem = sizeof(A22Smem);
-  KTG_CUDA(cudaFuncSetAttribute(k_support_a22, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e->a22_smem));
+  e->a22_smem = 0;  // static shared memory (sizeof(A22Smem) < 48 KB)
   int per_sm_a = 0;
   KTG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_a, k_support_a22, kSupportThreads, e->a22_smem));
   e->a22_grid = std::max(1, per_sm_a) * e->num_sms;
@@ -896,7 +897,8 @@ ktg_status begin_run(ktg_engine* e, uint32_t k, int parity) {
     parity = 0;
   }
   k_begin<<<1, 1, 0, e->stream>>>(e->d_st, k >= 2 ? k - 2 : 0, e->opt.width_bits == 16 ? 1 : 0, parity,
-                                  e->inc_active ? 1u : 0u, e->delta_ratio);
+                                  e->inc_active ? 1u : 0u, e->delta_ratio,
+                                  e->delta_ratio0);
   if (e->inc_active && e->pristine) {
     if (!flag(e, KTG_FLAG_NO_DEGREE_BOUND))
       k_heavy_rank<<<1, 1, 0, e->stream>>>(e->d_st, e->sym_deg_p.p, e->wl.n);
@@ -1040,7 +1042,7 @@ ktg_status support_pass(ktg_engine* e, int parity, uint64_t* triangles, bool max
   Layout& L = e->act();
   Graph g = e->graph_of(L);
   e->inc_active = false;
-  k_begin<<<1, 1, 0, e->stream>>>(e->d_st, 0, e->opt.width_bits == 16 ? 1 : 0, parity, 0u, e->delta_ratio);
+  k_begin<<<1, 1, 0, e->stream>>>(e->d_st, 0, e->opt.width_bits == 16 ? 1 : 0, parity, 0u, e->delta_ratio, e->delta_ratio0);
   k_plan_count<<<(L.nchunks + 255) / 256, 256, 0, e->stream>>>(g, 0);
   k_plan_write<<<1, 1024, 0, e->stream>>>(g);
   if (flag(e, KTG_FLAG_NAIVE_SUPPORT))

@@ -67,6 +67,7 @@ struct DevState {
   unsigned int last_carry;           //   queued delta pieces, whether it carried,
   unsigned long long last_dcost;     //   its delta cost and keep cost
   unsigned long long last_kcost;
+  double delta_ratio0;               // the same for round 0 of a run from the pristine graph
 };
 
 struct Graph {
@@ -716,10 +717,14 @@ k_support_chunked(Graph g) {
 // never needs rebuilding as rounds prune. A triangle (i, j, c) adds 1 to the
 // A22 slot (j, c) and the pivot (i, j) in shared memory and red.adds the tail
 // slot (i, c) once. Tasks are (chunk, batch of kA22Batch pivots), static.
+#ifndef KTG_A22_UNROLL
+#define KTG_A22_UNROLL 4
+#endif
 constexpr int kA22Batch = 256;
 constexpr int kA22TableBits = 11;          // 2048 slots for <= 512 entries (load <= 0.25)
 constexpr int kA22Strip = 256;             // flat tail elements a warp takes per grab
 constexpr int kA22Table = 1 << kA22TableBits;
+constexpr int kA22Unroll = KTG_A22_UNROLL;     // tail elements per lane per step (loads in flight)
 constexpr int kA22FiltWords = 512;         // 16K filter bits for <= 512 entries (~3% false positives)
 
 struct A22 {
@@ -759,8 +764,8 @@ __device__ __forceinline__ uint32_t a22_fbit(uint32_t h) { return (h ^ (h >> 15)
 __global__ void __launch_bounds__(kSupportThreads)
 k_support_a22(Graph g, Sym y, A22 a) {
   if (g.st->mode) return;  // supports carried this round
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  A22Smem& s = *reinterpret_cast<A22Smem*>(smem_raw);
+  // static (not dynamic) shared memory: constant-offset LDS addressing
+  __shared__ __align__(16) A22Smem s;
   const uint32_t tid = threadIdx.x;
   const int lane = tid & 31, wid = tid >> 5;
   constexpr int NW = kSupportThreads / 32;
@@ -912,20 +917,10 @@ k_support_a22(Graph g, Sym y, A22 a) {
         p = 8 * g + c2;
       }
       uint32_t pe_ = s.pref[p + 1], pb = s.pref[p], plo = s.plo[p], prun = s.prun[p];
-      for (uint32_t f = base + lane; f < lim; f += 32) {
-        if (f >= pe_) {
-          do {
-            ++p;
-            pe_ = s.pref[p + 1];
-          } while (pe_ <= f);
-          pb = s.pref[p];
-          plo = s.plo[p];
-          prun = s.prun[p];
-        }
-        const uint32_t slot = plo + (f - pb);
-        const uint32_t c = col[slot];
-        const uint32_t tb = prun >> 16, te = prun & 0xffffu;
-        // (value, run) lookup: the value may also sit in other rows' runs
+      // (value, run) lookup of tail element c of pivot pp: the value may also
+      // sit in other rows' runs
+      auto probe = [&](uint32_t c, uint32_t slot, uint32_t run, uint32_t pp) {
+        const uint32_t tb = run >> 16, te = run & 0xffffu;
         const uint32_t hh = a22_mix(c, te);
         const uint32_t fb = a22_fbit(hh);
         if (s.filt[fb >> 5] & (1u << (fb & 31))) {
@@ -941,10 +936,36 @@ k_support_a22(Graph g, Sym y, A22 a) {
           if (x < (uint32_t)kChunk) {
             atomicAdd(&s.cntA[x], 1u);
             atomicAdd(&S[slot], 1u);
-            atomicAdd(&s.cntP[p], 1u);
+            atomicAdd(&s.cntP[pp], 1u);
             ++tri_task;
           }
         }
+      };
+      auto advance = [&](uint32_t f) {
+        if (f >= pe_) {
+          do {
+            ++p;
+            pe_ = s.pref[p + 1];
+          } while (pe_ <= f);
+          pb = s.pref[p];
+          plo = s.plo[p];
+          prun = s.prun[p];
+        }
+      };
+      // kA22Unroll elements per lane per step, every load issued before any probe
+      for (uint32_t f = base + lane; f < lim; f += 32 * kA22Unroll) {
+        uint32_t sl[kA22Unroll], ru[kA22Unroll], pv[kA22Unroll], cv[kA22Unroll];
+#pragma unroll
+        for (int u = 0; u < kA22Unroll; ++u) {
+          const uint32_t fu = f + 32 * u;
+          if (fu < lim) advance(fu);
+          sl[u] = plo + (fu - pb), ru[u] = prun, pv[u] = p;
+        }
+#pragma unroll
+        for (int u = 0; u < kA22Unroll; ++u) cv[u] = (f + 32 * u < lim) ? col[sl[u]] : 0u;
+#pragma unroll
+        for (int u = 0; u < kA22Unroll; ++u)
+          if (f + 32 * u < lim) probe(cv[u], sl[u], ru[u], pv[u]);
       }
     }
     tri_local += tri_task;
@@ -1421,7 +1442,7 @@ __global__ void k_set_pristine(DevState* st) { st->pristine = 1; }
 __global__ void k_decide(DevState* st) {
   if (st->mode == 1) st->keep_cost = st->live_cost > st->delta_cost ? st->live_cost - st->delta_cost : 0;
   st->carry = (st->inc && st->removed != 0 &&
-               (double)st->delta_cost <= st->delta_ratio * (double)st->keep_cost)
+               (double)st->delta_cost <= (st->pristine ? st->delta_ratio0 : st->delta_ratio) * (double)st->keep_cost)
                   ? 1u
                   : 0u;
 }
@@ -2107,7 +2128,7 @@ __global__ void k_scatter_live(Graph w, const uint32_t* __restrict__ col_pristin
 // Loop control
 // ---------------------------------------------------------------------------
 __global__ void k_begin(DevState* st, uint32_t threshold, uint32_t width16, int parity, uint32_t inc,
-                        double delta_ratio) {
+                        double delta_ratio, double delta_ratio0) {
   st->inc = inc;
   st->mode = 0;
   st->nrq = 0;
@@ -2120,6 +2141,7 @@ __global__ void k_begin(DevState* st, uint32_t threshold, uint32_t width16, int 
   st->pristine = 0;
   st->live_cost = 0;
   st->delta_ratio = delta_ratio;
+  st->delta_ratio0 = delta_ratio0;
   st->sum_s = 0;
   st->delta_cost = 0;
   st->keep_cost = 0;
