@@ -185,7 +185,7 @@ struct ktg_engine {
   bool inc_active = false;    // the current fixpoint carries supports
   bool pristine = false;      // the working layout holds the pristine graph (after load / reset)
   double delta_ratio = 0.0625;  // carry when delta_cost <= ratio * keep_cost (s20 sweep calibration, scripts/ratio_scan.py)
-  double delta_ratio0 = 0.0625; // the same for round 0 from the pristine graph
+  double delta_ratio0 = 0.03;   // the same for round 0 from the pristine graph (same calibration)
 
   unsigned long long* d_workL = nullptr;
   DevState* d_st = nullptr;
