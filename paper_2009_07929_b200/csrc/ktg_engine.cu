@@ -157,7 +157,7 @@ struct ktg_engine {
   bool caller_stale = false;
 
   // reorientation / statistics scratch
-  DBuf<uint32_t> din, rank, offs, cntw, sizes, vals, vals_sorted;
+  DBuf<uint32_t> din, rank, offs, cntw, sizes, vals, vals_sorted, symdeg_w;
   DBuf<unsigned long long> keys, keys_sorted, ex_offs;
   DBuf<unsigned char> cub_tmp;
   DBuf<uint32_t> ex_out;
@@ -261,7 +261,8 @@ struct ktg_engine {
     exec = nullptr;
     cl.release();
     wl.release();
-    for (DBuf<uint32_t>* b : {&din, &rank, &offs, &cntw, &sizes, &vals, &vals_sorted, &ex_out}) b->release();
+    for (DBuf<uint32_t>* b : {&din, &rank, &offs, &cntw, &sizes, &vals, &vals_sorted, &symdeg_w, &ex_out})
+      b->release();
     keys.release();
     keys_sorted.release();
     ex_offs.release();
@@ -361,7 +362,8 @@ __global__ void k_clear_heavy(DevState* st) { st->nheavy = 0; }
 
 // Per-layout structures once L.row_ptr / L.col hold a CSR: live degrees,
 // chunk rows, off-diagonal task capacity, pristine copies.
-ktg_status prepare_layout(ktg_engine* e, Layout& L, bool keep_pristine) {
+ktg_status prepare_layout(ktg_engine* e, Layout& L, bool keep_pristine, const uint32_t* known_deg = nullptr,
+                          uint64_t known_live = 0) {
   const size_t nb = (size_t)L.n + 2;
   const size_t sb = L.slots + 4;  // +16 B: vector-load padding
   L.nchunks = (uint32_t)((L.slots + kChunk - 1) / kChunk);
@@ -375,9 +377,14 @@ ktg_status prepare_layout(ktg_engine* e, Layout& L, bool keep_pristine) {
   KTG_CUDA(cudaMemsetAsync(L.col.p + L.slots, 0, 16, e->stream));
   KTG_CUDA(cudaMemsetAsync(L.S0.p, 0, sb * 4, e->stream));
   KTG_CUDA(cudaMemsetAsync(L.S1.p, 0, sb * 4, e->stream));
-  KTG_CUDA(cudaMemsetAsync(L.deg.p, 0, nb * 4, e->stream));
   KTG_CUDA(cudaMemsetAsync(e->d_st, 0, sizeof(DevState), e->stream));
-  k_init_deg<<<4 * e->num_sms, 256, 0, e->stream>>>(L.row_ptr.p, L.col.p, L.n, L.slots, L.deg.p, e->d_st);
+  if (known_deg) {  // the builder counted every row (working layout: out-degrees)
+    KTG_CUDA(cudaMemcpyAsync(L.deg.p, known_deg, nb * 4, cudaMemcpyDeviceToDevice, e->stream));
+    k_set_live<<<1, 1, 0, e->stream>>>(e->d_st, known_live);
+  } else {
+    KTG_CUDA(cudaMemsetAsync(L.deg.p, 0, nb * 4, e->stream));
+    k_row_deg<<<(L.n + 255) / 256, 256, 0, e->stream>>>(L.row_ptr.p, L.col.p, L.n, L.deg.p, e->d_st);
+  }
   k_chunk_rows<<<(L.nchunks + 255) / 256, 256, 0, e->stream>>>(L.row_ptr.p, L.n, L.slots, L.nchunks,
                                                               L.chunk_row.p);
   KTG_CUDA(cudaGetLastError());
@@ -403,8 +410,12 @@ ktg_status prepare_layout(ktg_engine* e, Layout& L, bool keep_pristine) {
   return KTG_OK;
 }
 
-// Degree-ordered working layout from the caller layout's current state.
-ktg_status build_working(ktg_engine* e) {
+ktg_status sym_alloc(ktg_engine* e, uint64_t m);
+
+// Degree-ordered working layout from the caller layout's current state; with
+// `with_sym` (carried-support runs) the same pass also writes the symmetric
+// rows, pos_of/erow and the A22 in-edge list (build_sym finishes them).
+ktg_status build_working(ktg_engine* e, bool with_sym) {
   Layout& C = e->cl;
   Layout& W = e->wl;
   const uint32_t n = C.n;
@@ -421,6 +432,7 @@ ktg_status build_working(ktg_engine* e) {
   KTG_TRY(e->offs.ensure(nb));
   KTG_TRY(e->cntw.ensure(nb));
   KTG_TRY(e->sizes.ensure(nb));
+  KTG_TRY(e->symdeg_w.ensure(nb));
   KTG_TRY(e->keys.ensure(std::max<uint64_t>(m, n)));
   KTG_TRY(e->keys_sorted.ensure(std::max<uint64_t>(m, n)));
   KTG_TRY(e->vals.ensure(m));
@@ -430,6 +442,7 @@ ktg_status build_working(ktg_engine* e) {
   // undirected degree = out (deg) + in (din)
   KTG_CUDA(cudaMemsetAsync(e->din.p, 0, nb * 4, s));
   KTG_CUDA(cudaMemsetAsync(e->cntw.p, 0, nb * 4, s));
+  KTG_CUDA(cudaMemsetAsync(e->symdeg_w.p, 0, nb * 4, s));
   k_work_din<<<e->prune_grid, kPruneThreads, 0, s>>>(g, e->din.p);
   k_rank_keys<<<4 * e->num_sms, 256, 0, s>>>(C.deg.p, e->din.p, n, e->keys.p);
   KTG_CUDA(cudaGetLastError());
@@ -443,11 +456,22 @@ ktg_status build_working(ktg_engine* e) {
   KTG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp2, e->keys.p, e->keys_sorted.p, e->vals.p,
                                            e->vals_sorted.p, (int64_t)m, 0, 2 * B, s));
   KTG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp3, e->sizes.p, W.row_ptr.p, (int)nb, s));
-  KTG_TRY(e->cub_tmp.ensure(std::max(tmp, std::max(tmp2, tmp3))));
+  tmp = std::max(tmp, std::max(tmp2, tmp3));
+  if (with_sym) {
+    size_t t4 = 0, t5 = 0;
+    KTG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, t4, (unsigned long long*)nullptr, (unsigned long long*)nullptr,
+                                           (int)nb, s));
+    // in-lists: a STABLE sort of the working edges (emitted in (a, b) order)
+    // by b alone keeps every in-list ascending in a -- B key bits, not 2B
+    KTG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, t5, e->vals.p, e->vals_sorted.p, e->keys.p,
+                                             e->keys_sorted.p, (int64_t)m, 0, (int)B, s));
+    tmp = std::max(tmp, std::max(t4, t5));
+  }
+  KTG_TRY(e->cub_tmp.ensure(tmp));
   tmp = e->cub_tmp.cap;
   KTG_CUDA(cub::DeviceRadixSort::SortKeys(e->cub_tmp.p, tmp, e->keys.p, e->keys_sorted.p, (int)n, 0,
                                           32 + deg_bits, s));
-  k_rank_assign<<<4 * e->num_sms, 256, 0, s>>>(e->keys_sorted.p, n, e->rank.p);
+  k_rank_assign<<<4 * e->num_sms, 256, 0, s>>>(e->keys_sorted.p, n, e->rank.p, e->symdeg_w.p);
   // edge keys in caller row order, then sort by (a, b)
   tmp = e->cub_tmp.cap;
   KTG_CUDA(cub::DeviceScan::ExclusiveSum(e->cub_tmp.p, tmp, C.deg.p, e->offs.p, (int)nb, s));
@@ -462,9 +486,32 @@ ktg_status build_working(ktg_engine* e) {
   tmp = e->cub_tmp.cap;
   KTG_CUDA(cub::DeviceScan::ExclusiveSum(e->cub_tmp.p, tmp, e->sizes.p, W.row_ptr.p, (int)nb, s));
   KTG_CUDA(cudaMemsetAsync(W.col.p, 0, W.slots * 4, s));
-  k_fill_working<<<8 * e->num_sms, 256, 0, s>>>(e->keys_sorted.p, e->vals_sorted.p, m, B, W.col.p, W.id.p);
+  if (!with_sym) {
+    k_fill_working<<<8 * e->num_sms, 256, 0, s>>>(e->keys_sorted.p, e->vals_sorted.p, m, B, W.col.p, W.id.p);
+    KTG_CUDA(cudaGetLastError());
+    return prepare_layout(e, W, true, e->cntw.p, m);
+  }
+  KTG_TRY(sym_alloc(e, m));
+  unsigned long long* sz = e->sym_sizes.p;  // [tot | din | - | inoff | -] x nb
+  k_sym_sizes<<<4 * e->num_sms, 256, 0, s>>>(e->symdeg_w.p, e->cntw.p, n, e->din.p, sz);
+  tmp = e->cub_tmp.cap;
+  KTG_CUDA(cub::DeviceScan::ExclusiveSum(e->cub_tmp.p, tmp, sz, e->sym_ptr.p, (int)nb, s));
+  tmp = e->cub_tmp.cap;
+  KTG_CUDA(cub::DeviceScan::ExclusiveSum(e->cub_tmp.p, tmp, sz + nb, sz + 3 * nb, (int)nb, s));
+  KTG_CUDA(cudaMemsetAsync(e->d_workL, 0, 8, s));
+  Sym y = e->sym();
+  k_fill_all<<<8 * e->num_sms, 256, 0, s>>>(e->keys_sorted.p, e->vals_sorted.p, m, B, W.row_ptr.p, W.col.p,
+                                            W.id.p, e->din.p, e->symdeg_w.p, y, e->vals.p, e->keys.p,
+                                            e->d_workL);
   KTG_CUDA(cudaGetLastError());
-  return prepare_layout(e, W, true);
+  tmp = e->cub_tmp.cap;
+  KTG_CUDA(cub::DeviceRadixSort::SortPairs(e->cub_tmp.p, tmp, e->vals.p, e->vals_sorted.p, e->keys.p,
+                                           e->keys_sorted.p, (int64_t)m, 0, (int)B, s));
+  k_fill_in_all<<<8 * e->num_sms, 256, 0, s>>>(e->vals_sorted.p, e->keys_sorted.p, m, sz + 3 * nb, W.id.p, y,
+                                               e->a22_pe.p, e->a22_pin.p);
+  KTG_CUDA(cudaGetLastError());
+  KTG_CUDA(cudaMemcpyAsync(e->sym_deg.p, e->symdeg_w.p, nb * 4, cudaMemcpyDeviceToDevice, s));
+  return prepare_layout(e, W, true, e->cntw.p, m);
 }
 
 // Static structures of the A22-staged support pass (after build_sym): the
@@ -482,9 +529,8 @@ ktg_status build_a22(ktg_engine* e) {
   KTG_TRY(e->a22_jfirst.ensure(Q));
   KTG_TRY(e->a22_cnt.ensure((size_t)Q + 1));
   Sym y = e->sym();
-  // a22_pe (the sorted in-list ids) was written by k_sym_fill_in
+  // a22_pe (the sorted in-list ids) and a22_pin were written by k_fill_in_all
   k_u64_to_u32<<<4 * e->num_sms, 256, 0, s>>>(e->sym_sizes.p + 3 * nb, (uint32_t)nb, e->a22_off.p);
-  k_a22_pin<<<4 * e->num_sms, 256, 0, s>>>(e->a22_pe.p, m, y, e->a22_pin.p);
   k_chunk_first<<<(Q + 255) / 256, 256, 0, s>>>(W.row_ptr.p, n, W.slots, Q, e->a22_jfirst.p);
   k_a22_count<<<(Q + 256) / 256, 256, 0, s>>>(e->a22_jfirst.p, W.chunk_row.p, e->a22_off.p, Q, e->a22_cnt.p);
   KTG_CUDA(cudaGetLastError());
@@ -504,17 +550,13 @@ ktg_status build_a22(ktg_engine* e) {
   return KTG_OK;
 }
 
-// Symmetric adjacency of the (pristine) working layout for incremental
-// rounds: row v = sorted in-neighbours ++ out-neighbours (working row v), each
-// with the edge id; pos_of; pristine copies; the delta queue.
-ktg_status build_sym(ktg_engine* e) {
-  Layout& W = e->wl;
-  const uint32_t n = W.n;
-  const uint64_t m = W.live_pristine;
-  const size_t nb = (size_t)n + 2;
-  const cudaStream_t s = e->stream;
+// Buffers of the symmetric adjacency (build_working fills them when it
+// builds with_sym): row v = sorted in-neighbours ++ out-neighbours (working
+// row v), each with the edge id; pos_of / erow per edge id; the A22 in-edge
+// list and its pristine {slot, row} records.
+ktg_status sym_alloc(ktg_engine* e, uint64_t m) {
+  const size_t nb = (size_t)e->cl.n + 2;
   e->sym_ready = false;
-  if (n > 0x7fffffffu) return KTG_OK;  // col marks need the top bit
   e->sym_entries = 2 * m;
   KTG_TRY(e->sym_ptr.ensure(nb));
   KTG_TRY(e->sym_sizes.ensure(5 * nb));
@@ -535,48 +577,18 @@ ktg_status build_sym(ktg_engine* e) {
   KTG_TRY(e->pos_of_p.ensure(e->cl.slots));
   KTG_TRY(e->erow.ensure(e->cl.slots));
   KTG_TRY(e->dead.ensure(e->cl.slots));
-  KTG_TRY(e->din.ensure(nb));
-  KTG_TRY(e->keys.ensure(std::max<uint64_t>(m, n)));
-  KTG_TRY(e->keys_sorted.ensure(std::max<uint64_t>(m, n)));
-  KTG_TRY(e->vals.ensure(m));
-  KTG_TRY(e->vals_sorted.ensure(m));
-  Graph g = e->graph_of(W);
-  unsigned long long* sz = e->sym_sizes.p;  // [tot | din | dout | inoff | outoff] x nb
-  KTG_CUDA(cudaMemsetAsync(e->din.p, 0, nb * 4, s));
-  k_work_din<<<e->prune_grid, kPruneThreads, 0, s>>>(g, e->din.p);
-  k_u32_to_u64<<<4 * e->num_sms, 256, 0, s>>>(e->din.p, (uint32_t)nb, sz + nb);
-  k_u32_to_u64<<<4 * e->num_sms, 256, 0, s>>>(W.deg.p, (uint32_t)nb, sz + 2 * nb);
-  KTG_CUDA(cudaGetLastError());
-  size_t tmp = 0, tmp2 = 0;
-  KTG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, sz, e->sym_ptr.p, (int)nb, s));
-  uint32_t B = 1;
-  while ((1ull << B) <= n) ++B;
-  // in-lists: a STABLE sort of the working edges (emitted in (u, v) order)
-  // by v alone keeps every in-list ascending in u -- B key bits, not 2B
-  KTG_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, tmp2, e->vals.p, e->vals_sorted.p, e->keys.p,
-                                           e->keys_sorted.p, (int64_t)m, 0, (int)B, s));
-  KTG_TRY(e->cub_tmp.ensure(std::max(tmp, tmp2)));
-  // tot = din + dout (one add kernel via the scan of the two halves)
-  k_add_u64<<<4 * e->num_sms, 256, 0, s>>>(sz + nb, sz + 2 * nb, (uint32_t)nb, sz);
-  tmp = e->cub_tmp.cap;
-  KTG_CUDA(cub::DeviceScan::ExclusiveSum(e->cub_tmp.p, tmp, sz, e->sym_ptr.p, (int)nb, s));
-  tmp = e->cub_tmp.cap;
-  KTG_CUDA(cub::DeviceScan::ExclusiveSum(e->cub_tmp.p, tmp, sz + nb, sz + 3 * nb, (int)nb, s));
-  tmp = e->cub_tmp.cap;
-  KTG_CUDA(cub::DeviceScan::ExclusiveSum(e->cub_tmp.p, tmp, sz + 2 * nb, sz + 4 * nb, (int)nb, s));
-  k_sym_in_keys<<<e->prune_grid, kPruneThreads, 0, s>>>(g, e->vals.p, e->keys.p, sz + 4 * nb);
-  KTG_CUDA(cudaGetLastError());
-  tmp = e->cub_tmp.cap;
-  KTG_CUDA(cub::DeviceRadixSort::SortPairs(e->cub_tmp.p, tmp, e->vals.p, e->vals_sorted.p, e->keys.p,
-                                           e->keys_sorted.p, (int64_t)m, 0, (int)B, s));
-  Sym y = e->sym();
   KTG_TRY(e->a22_pe.ensure(m));
-  k_sym_fill_in<<<8 * e->num_sms, 256, 0, s>>>(e->vals_sorted.p, e->keys_sorted.p, m, sz + 3 * nb, y,
-                                               e->a22_pe.p);
-  k_sym_fill_out<<<e->prune_grid, kPruneThreads, 0, s>>>(g, e->din.p, y);
-  KTG_CUDA(cudaMemsetAsync(e->d_workL, 0, 8, s));
-  k_sym_pos<<<e->prune_grid, kPruneThreads, 0, s>>>(g, y, e->d_workL);
-  KTG_CUDA(cudaGetLastError());
+  KTG_TRY(e->a22_pin.ensure(m));
+  return KTG_OK;
+}
+
+// Finishes the symmetric adjacency written by build_working(with_sym):
+// pristine copies, per-round flags, the delta queue capacity k_fill_all
+// totalled, then the A22 plan.
+ktg_status build_sym(ktg_engine* e) {
+  const uint64_t m = e->wl.live_pristine;
+  const size_t nb = (size_t)e->cl.n + 2;
+  const cudaStream_t s = e->stream;
   KTG_CUDA(cudaMemcpyAsync(e->sym_nbr_p.p, e->sym_nbr.p, 2 * m * 4, cudaMemcpyDeviceToDevice, s));
   KTG_CUDA(cudaMemcpyAsync(e->sym_eid_p.p, e->sym_eid.p, 2 * m * 4, cudaMemcpyDeviceToDevice, s));
   KTG_CUDA(cudaMemcpyAsync(e->sym_deg_p.p, e->sym_deg.p, nb * 4, cudaMemcpyDeviceToDevice, s));
@@ -592,8 +604,24 @@ ktg_status build_sym(ktg_engine* e) {
   e->sym_ready = true;
   e->pristine = true;
   return build_a22(e);
-  return KTG_OK;
 }
+
+// KTG_LOAD_TIMING=1: per-phase wall times of the host-buffer path on stderr
+// (debug; synchronises the stream at every mark, so never on in a benchmark).
+struct PhaseTimer {
+  cudaStream_t s;
+  bool on;
+  double last = 0;
+  explicit PhaseTimer(cudaStream_t st) : s(st), on(getenv("KTG_LOAD_TIMING") != nullptr) {}
+  void operator()(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    const double now =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    if (last != 0) fprintf(stderr, "ktg: %-28s %8.3f ms\n", what, now - last);
+    last = now;
+  }
+};
 
 // Uploads (host or device source) into the caller layout; builds the working
 // layout unless the label order is requested. Buffers are reused when the
@@ -615,15 +643,7 @@ ktg_status engine_load(ktg_engine* e, const uint32_t* row_ptr, uint32_t n, const
   e->caller_stale = false;
   KTG_TRY(C.row_ptr.ensure((size_t)n + 2));
   KTG_TRY(C.col.ensure(slots + 4));
-  // KTG_LOAD_TIMING=1: per-phase wall times of the load on stderr (debug)
-  static const bool timing = getenv("KTG_LOAD_TIMING") != nullptr;
-  std::vector<std::pair<const char*, double>> marks;
-  auto mark = [&](const char* what) {
-    if (!timing) return;
-    cudaStreamSynchronize(e->stream);
-    marks.emplace_back(what, std::chrono::duration<double, std::milli>(
-                                 std::chrono::steady_clock::now().time_since_epoch()).count());
-  };
+  PhaseTimer mark(e->stream);
   mark("start");
   if (row_ptr) KTG_CUDA(cudaMemcpyAsync(C.row_ptr.p, row_ptr, ((size_t)n + 2) * 4, kind, e->stream));
   if (col) KTG_CUDA(cudaMemcpyAsync(C.col.p, col, slots * 4, kind, e->stream));
@@ -631,13 +651,14 @@ ktg_status engine_load(ktg_engine* e, const uint32_t* row_ptr, uint32_t n, const
   KTG_TRY(prepare_layout(e, C, keep_pristine || e->reoriented));
   mark("caller layout");
   if (e->reoriented) {
-    KTG_TRY(build_working(e));
-    mark("working layout");
-    if (!flag(e, KTG_FLAG_RECOMPUTE)) KTG_TRY(build_sym(e));
-    mark("symmetric rows + A22 plan");
+    // carried-support runs need the symmetric rows (col marks use the top bit)
+    const bool with_sym = !flag(e, KTG_FLAG_RECOMPUTE) && n <= 0x7fffffffu;
+    e->sym_ready = false;
+    KTG_TRY(build_working(e, with_sym));
+    mark("working layout (+ symmetric rows)");
+    if (with_sym) KTG_TRY(build_sym(e));
+    mark("A22 plan");
   }
-  for (size_t i = 1; i < marks.size(); ++i)
-    fprintf(stderr, "ktg load: %-26s %8.3f ms\n", marks[i].first, marks[i].second - marks[i - 1].second);
   return KTG_OK;
 }
 
@@ -1068,7 +1089,10 @@ ktg_status support_pass(ktg_engine* e, int parity, uint64_t* triangles, bool max
 }
 
 ktg_status extract(ktg_engine* e, uint32_t* u, uint32_t* v, uint32_t* s, uint64_t cap, uint64_t* num) {
+  PhaseTimer mark(e->stream);
+  mark("start");
   KTG_TRY(publish(e));
+  mark("extract: publish");
   KTG_TRY(read_state(e));
   Layout& C = e->cl;
   const uint64_t live = e->h_st->live;
@@ -1089,10 +1113,12 @@ ktg_status extract(ktg_engine* e, uint32_t* u, uint32_t* v, uint32_t* s, uint64_
   k_extract<<<e->prune_grid, kPruneThreads, 0, e->stream>>>(e->graph_of(C), caller_S(e), e->ex_offs.p, out,
                                                            out + live, out + 2 * live);
   KTG_CUDA(cudaGetLastError());
+  mark("extract: compaction");
   KTG_CUDA(cudaMemcpyAsync(u, out, live * 4, cudaMemcpyDeviceToHost, e->stream));
   KTG_CUDA(cudaMemcpyAsync(v, out + live, live * 4, cudaMemcpyDeviceToHost, e->stream));
   KTG_CUDA(cudaMemcpyAsync(s, out + 2 * live, live * 4, cudaMemcpyDeviceToHost, e->stream));
   KTG_CUDA(cudaStreamSynchronize(e->stream));
+  mark("extract: D2H");
   return KTG_OK;
 }
 
@@ -1546,11 +1572,16 @@ ktg_status ktg_ktruss(const uint32_t* row_ptr, uint32_t n, const uint32_t* col_i
   TmpEngine t;
   KTG_TRY(tmp_engine(opt, row_ptr, n, col_idx, slots, false, true, t));
   ktg_engine* e = t.e;
+  PhaseTimer mark(e->stream);
+  mark("start");
   KTG_TRY(begin_run(e, k, 0));
   KTG_TRY(run_loop(e, true));
   KTG_TRY(finish_info(e));
   KTG_TRY(copy_hist(e, removed_hist, hist_cap, iterations));
-  return extract(e, out_u, out_v, out_support, edge_cap, num_edges);
+  mark("ktruss: fixpoint");
+  const ktg_status st = extract(e, out_u, out_v, out_support, edge_cap, num_edges);
+  mark("ktruss: publish + extract");
+  return st;
 }
 
 ktg_status ktg_kmax_search(const uint32_t* row_ptr, uint32_t n, const uint32_t* col_idx, uint64_t slots,

@@ -126,37 +126,32 @@ __device__ __forceinline__ uint32_t* other_S(const Graph& g) { return g.st->pari
 // Setup kernels
 // ---------------------------------------------------------------------------
 
-// Live out-degree of every row and the live total, slot-parallel: the last
-// live slot of a row is a nonzero followed by a zero (rows are zero-prefix-
-// free and end in a zero, csr.hpp:12-16), so each row is found once with a
-// binary search over row_ptr. deg must be zeroed (rows with no live slot).
-__global__ void k_init_deg(const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ col,
-                           uint32_t n, uint64_t slots, uint32_t* __restrict__ deg, DevState* st) {
+// validate_csr (csr.cpp:34-80) per-row checks on the device, warp per row:
+// first violation in reference order, packed row << 3 | code into *first
+// (atomicMin keeps the lowest row). Codes: 1 no sentinel slot, 2 no zero at
+// the row end, 3 nonzero after a zero, 4 not strictly ascending above the
+// vertex, 5 beyond n.
+// Live out-degree per row, thread per row: a valid row is nonzeros then
+// zeros, so its first zero is found by a binary search inside the row
+// (O(n log d) instead of a search over row_ptr per row end).
+__global__ void k_row_deg(const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ col, uint32_t n,
+                          uint32_t* __restrict__ deg, DevState* st) {
   unsigned long long live = 0;
-  for (uint64_t s = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; s + 1 < slots;
-       s += (uint64_t)gridDim.x * blockDim.x) {
-    if (col[s] != 0 && col[s + 1] == 0) {
-      uint32_t lo = 0, hi = n + 2;
-      while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (row_ptr[mid] <= (uint32_t)s) lo = mid + 1; else hi = mid;
-      }
-      const uint32_t row = lo - 1;
-      const uint32_t d = (uint32_t)s - row_ptr[row] + 1;
-      deg[row] = d;
-      live += d;
+  for (uint32_t v = blockIdx.x * blockDim.x + threadIdx.x + 1; v <= n; v += gridDim.x * blockDim.x) {
+    uint32_t lo = row_ptr[v], hi = row_ptr[v + 1];
+    const uint32_t b = lo;
+    while (lo < hi) {  // first zero in [lo, hi)
+      const uint32_t mid = (lo + hi) >> 1;
+      if (col[mid] != 0) lo = mid + 1; else hi = mid;
     }
+    deg[v] = lo - b;
+    live += lo - b;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) live += __shfl_xor_sync(0xffffffffu, live, o);
   if ((threadIdx.x & 31) == 0 && live) atomicAdd(&st->live, live);
 }
 
-// validate_csr (csr.cpp:34-80) per-row checks on the device, warp per row:
-// first violation in reference order, packed row << 3 | code into *first
-// (atomicMin keeps the lowest row). Codes: 1 no sentinel slot, 2 no zero at
-// the row end, 3 nonzero after a zero, 4 not strictly ascending above the
-// vertex, 5 beyond n.
 __global__ void k_validate_rows(const uint32_t* __restrict__ row_ptr, const uint32_t* __restrict__ col, uint32_t n,
                                 uint64_t slots, unsigned long long* first) {
   const int lane = threadIdx.x & 31;
@@ -987,14 +982,6 @@ k_support_a22(Graph g, Sym y, A22 a) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) tri_local += __shfl_xor_sync(0xffffffffu, tri_local, o);
   if (lane == 0 && tri_local) atomicAdd(&g.st->triangles, tri_local);
-}
-
-// Load time: pristine {slot, row} of every pivot of the in-edge list.
-__global__ void k_a22_pin(const uint32_t* __restrict__ pe, uint64_t m, Sym y, uint2* __restrict__ pin_p) {
-  for (uint64_t k = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; k < m; k += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t id = pe[k];
-    pin_p[k] = make_uint2(y.pos_of[id], y.erow[id]);
-  }
 }
 
 // Load time: row holding each chunk's first slot.
@@ -1900,90 +1887,8 @@ __global__ void k_inc_triangles_done(DevState* st) {
   st->sum_s = 0;
 }
 
-// Symmetric adjacency build (load time). For every live working edge u -> v
-// (emitted in working (u, v) order): key v, value u << 32 | id. A stable sort
-// by v leaves each in-list ascending in u.
-__global__ void k_sym_in_keys(Graph w, uint32_t* __restrict__ keys, unsigned long long* __restrict__ vals,
-                              const unsigned long long* __restrict__ offs) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t u = warp + 1; u <= w.n; u += nwarps) {
-    const uint32_t d = w.deg[u], base = w.row_ptr[u];
-    const unsigned long long o = offs[u];
-    for (uint32_t x = lane; x < d; x += 32) {
-      keys[o + x] = w.col[base + x];
-      vals[o + x] = ((unsigned long long)u << 32) | w.payload[base + x];
-    }
-  }
-}
-
-// Element-parallel: sorted entry i of the in-lists goes to position
-// i - inoff[v] of symmetric row v (its in-part); its id is also the i-th
-// entry of the A22 in-edge list.
-__global__ void k_sym_fill_in(const uint32_t* __restrict__ vkeys, const unsigned long long* __restrict__ vals,
-                              uint64_t m, const unsigned long long* __restrict__ inoff, Sym y,
-                              uint32_t* __restrict__ pe) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t v = vkeys[i];
-    const unsigned long long pv = vals[i];
-    const unsigned long long dst = y.ptr[v] + (i - inoff[v]);
-    y.nbr[dst] = (uint32_t)(pv >> 32);
-    y.eid[dst] = (uint32_t)pv;
-    pe[i] = (uint32_t)pv;
-  }
-}
-
-// Out-part of symmetric row v = working row v (warp per row; working rows
-// are short in degree order); live length = in + out.
-__global__ void k_sym_fill_out(Graph w, const uint32_t* __restrict__ din, Sym y) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-  for (uint32_t v = warp + 1; v <= w.n; v += nwarps) {
-    const unsigned long long dst = y.ptr[v] + din[v];
-    const uint32_t d = w.deg[v], base = w.row_ptr[v];
-    for (uint32_t x = lane; x < d; x += 32) {
-      y.nbr[dst + x] = w.col[base + x];
-      y.eid[dst + x] = w.payload[base + x];
-    }
-    if (lane == 0) y.deg[v] = din[v] + d;
-  }
-}
-
-// pos_of for the pristine working layout, and the delta queue capacity: one
-// task per kDeltaPiece elements of min(du, dv) over every edge -- degrees only
-// shrink, so no round can queue more.
-__global__ void k_sym_pos(Graph w, Sym y, unsigned long long* __restrict__ cap) {
-  const int lane = threadIdx.x & 31;
-  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
-  unsigned long long c = 0;
-  for (uint32_t u = warp + 1; u <= w.n; u += nwarps) {
-    const uint32_t d = w.deg[u], base = w.row_ptr[u], du = y.deg[u];
-    for (uint32_t x = lane; x < d; x += 32) {
-      y.pos_of[w.payload[base + x]] = base + x;
-      const_cast<uint32_t*>(y.erow)[w.payload[base + x]] = u;
-      const uint32_t mn = min(du, y.deg[w.col[base + x]]);
-      c += (mn + kDeltaPiece - 1) / kDeltaPiece;
-    }
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-  if (lane == 0 && c) atomicAdd(cap, c);
-}
-
-__global__ void k_add_u64(const unsigned long long* __restrict__ a, const unsigned long long* __restrict__ b,
-                          uint32_t n, unsigned long long* __restrict__ c) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) c[i] = a[i] + b[i];
-}
-
 __global__ void k_u64_to_u32(const unsigned long long* __restrict__ a, uint32_t n, uint32_t* __restrict__ b) {
   for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) b[i] = (uint32_t)a[i];
-}
-
-__global__ void k_u32_to_u64(const uint32_t* __restrict__ a, uint32_t n, unsigned long long* __restrict__ b) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) b[i] = a[i];
 }
 
 // ---------------------------------------------------------------------------
@@ -2055,9 +1960,13 @@ __global__ void k_rank_keys(const uint32_t* __restrict__ deg, const uint32_t* __
     keys[v - 1] = ((unsigned long long)(deg[v] + din[v]) << 32) | v;
 }
 
-__global__ void k_rank_assign(const unsigned long long* __restrict__ sorted, uint32_t n, uint32_t* __restrict__ rank) {
-  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
-    rank[(uint32_t)sorted[i]] = i + 1;
+__global__ void k_rank_assign(const unsigned long long* __restrict__ sorted, uint32_t n, uint32_t* __restrict__ rank,
+                              uint32_t* __restrict__ symdeg_w) {
+  for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    const unsigned long long k = sorted[i];
+    rank[(uint32_t)k] = i + 1;
+    symdeg_w[i + 1] = (uint32_t)(k >> 32);  // undirected degree of rank i + 1
+  }
 }
 
 // Edge keys (a << B | b, a < b ranks) with the caller slot as value,
@@ -2070,7 +1979,9 @@ __global__ void k_edge_keys(Graph g, const uint32_t* __restrict__ rank, const ui
        x += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t c = g.col[x];
     if (c == 0) continue;
-    uint32_t lo = 0, hi = g.n + 2;  // row = upper_bound(row_ptr, x) - 1
+    // row = upper_bound(row_ptr, x) - 1, inside the rows of x's chunk
+    const uint32_t q = (uint32_t)(x / kChunk);
+    uint32_t lo = q ? g.chunk_row[q - 1] : 0u, hi = g.chunk_row[q] + 1;
     while (lo < hi) {
       const uint32_t mid = (lo + hi) >> 1;
       if (g.row_ptr[mid] <= (uint32_t)x) lo = mid + 1; else hi = mid;
@@ -2102,6 +2013,75 @@ __global__ void k_fill_working(const unsigned long long* __restrict__ keys, cons
     const uint64_t slot = i + a - 1;
     col_w[slot] = (uint32_t)(k & mask);
     id_w[slot] = vals[i];
+  }
+}
+
+// Working layout + symmetric rows in one pass (carried-support runs): per
+// rank r, din_w = undirected degree - out-degree; the u64 sizes for the
+// symmetric-row offsets (tot | din) scans.
+__global__ void k_sym_sizes(const uint32_t* __restrict__ symdeg_w, const uint32_t* __restrict__ cntw, uint32_t n,
+                            uint32_t* __restrict__ din_w, unsigned long long* __restrict__ sz) {
+  const uint32_t nb = n + 2;
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < nb; r += gridDim.x * blockDim.x) {
+    const uint32_t tot = (r >= 1 && r <= n) ? symdeg_w[r] : 0u;
+    const uint32_t dout = (r >= 1 && r <= n) ? cntw[r] : 0u;
+    din_w[r] = tot - dout;
+    sz[r] = tot;
+    sz[nb + r] = tot - dout;
+  }
+}
+
+// Sorted (a << B | b, caller slot) entry i of the working edges: writes the
+// working col/id, pos_of/erow of the edge id, the out-part of symmetric row
+// a, and the in-list key (b, a << 32 | working slot) of entry i (entries stay
+// in (a, b) order, so a stable sort by b alone yields ascending in-lists);
+// totals the delta queue capacity (one task per kDeltaPiece elements of
+// min(du, dv) per edge: degrees only shrink, so no round queues more).
+__global__ void k_fill_all(const unsigned long long* __restrict__ keys, const uint32_t* __restrict__ vals, uint64_t m,
+                           uint32_t B, const uint32_t* __restrict__ row_ptr_w, uint32_t* __restrict__ col_w,
+                           uint32_t* __restrict__ id_w, const uint32_t* __restrict__ din_w,
+                           const uint32_t* __restrict__ symdeg_w, Sym y, uint32_t* __restrict__ ikeys,
+                           unsigned long long* __restrict__ ivals, unsigned long long* __restrict__ cap) {
+  const unsigned long long mask = (1ull << B) - 1;
+  unsigned long long c = 0;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
+    const unsigned long long k = keys[i];
+    const uint32_t a = (uint32_t)(k >> B), b = (uint32_t)(k & mask);
+    const uint32_t id = vals[i];
+    const uint32_t slot = (uint32_t)(i + a - 1);
+    col_w[slot] = b;
+    id_w[slot] = id;
+    y.pos_of[id] = slot;
+    const_cast<uint32_t*>(y.erow)[id] = a;
+    const unsigned long long dst = y.ptr[a] + din_w[a] + (slot - row_ptr_w[a]);
+    y.nbr[dst] = b;
+    y.eid[dst] = id;
+    ikeys[i] = b;
+    ivals[i] = ((unsigned long long)a << 32) | slot;
+    c += (min(symdeg_w[a], symdeg_w[b]) + kDeltaPiece - 1) / kDeltaPiece;
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(cap, c);
+}
+
+// Sorted in-list entry i (key b, value a << 32 | working slot): position
+// i - inoff[b] of symmetric row b's in-part; also the i-th entry of the A22
+// in-edge list (edge id) and its pristine {slot, row} record.
+__global__ void k_fill_in_all(const uint32_t* __restrict__ vkeys, const unsigned long long* __restrict__ vals,
+                              uint64_t m, const unsigned long long* __restrict__ inoff,
+                              const uint32_t* __restrict__ id_w, Sym y, uint32_t* __restrict__ pe,
+                              uint2* __restrict__ pin_p) {
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t b = vkeys[i];
+    const unsigned long long pv = vals[i];
+    const uint32_t a = (uint32_t)(pv >> 32), slot = (uint32_t)pv;
+    const uint32_t id = id_w[slot];
+    const unsigned long long dst = y.ptr[b] + (i - inoff[b]);
+    y.nbr[dst] = a;
+    y.eid[dst] = id;
+    pe[i] = id;
+    pin_p[i] = make_uint2(slot, a);
   }
 }
 

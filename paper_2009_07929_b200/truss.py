@@ -18,6 +18,7 @@ from __future__ import annotations
 import ctypes
 import enum
 import os
+import sys
 from dataclasses import dataclass, field
 from typing import Callable, List, Optional
 
@@ -277,16 +278,63 @@ def _options(o: Optional[TrussOptions], keep=None) -> _Options:
     return c
 
 
-def _host_u32(count: int) -> np.ndarray:
-    """Output buffer for device->host copies: page-locked (PyTorch's caching
-    host allocator, so repeated calls do not re-pin) when CUDA is up."""
-    try:
-        import torch
-        if torch.cuda.is_available():
-            return torch.empty(max(count, 1), dtype=torch.int32, pin_memory=True).numpy().view(np.uint32)
-    except Exception:
-        pass
-    return np.empty(max(count, 1), np.uint32)
+class _ResultPool:
+    """Page-locked (u, v, support) result columns reused across calls.
+
+    Pinning fresh host memory per call costs more than the fixpoint itself
+    (cudaHostAlloc of ~190 MB at R-MAT s20 is ~7 ms), so each call borrows a
+    pooled buffer. A buffer is free again once no array viewing it is alive
+    (the refcount of the ndarray that owns the pinned pages). Results much
+    smaller than the buffer are copied out so a kept result does not pin a
+    whole buffer."""
+
+    MAX_POOLED = 4
+    COPY_OUT_BYTES = 4 << 20
+
+    def __init__(self):
+        self._owners = []
+
+    def take(self, cap: int):
+        words = 3 * max(cap, 1)
+        for owner in self._owners:
+            # refs: the pool list, this loop variable, getrefcount's argument
+            if owner.shape[0] >= words and sys.getrefcount(owner) <= 3:
+                return owner
+        owner = self._alloc(1 << max(20, (words - 1).bit_length()))  # power-of-two classes
+        if owner is None:
+            return np.empty(words, np.int32)
+        if len(self._owners) >= self.MAX_POOLED:  # drop the smallest free buffer
+            free = [i for i in range(len(self._owners)) if sys.getrefcount(self._owners[i]) <= 2]
+            if free:
+                del self._owners[min(free, key=lambda i: self._owners[i].shape[0])]
+        if len(self._owners) < self.MAX_POOLED:
+            self._owners.append(owner)
+        return owner
+
+    @staticmethod
+    def _alloc(size: int):
+        try:
+            import torch
+            if torch.cuda.is_available():
+                return torch.empty(size, dtype=torch.int32, pin_memory=True).numpy()
+        except Exception:
+            pass
+        return None
+
+    @staticmethod
+    def columns(owner, cap: int):
+        buf = owner.view(np.uint32)
+        cap = max(cap, 1)
+        return buf[:cap], buf[cap:2 * cap], buf[2 * cap:3 * cap]
+
+    @classmethod
+    def finish(cls, u, v, sup, m: int):
+        if 12 * m <= cls.COPY_OUT_BYTES:
+            return u[:m].copy(), v[:m].copy(), sup[:m].copy()
+        return u[:m], v[:m], sup[:m]
+
+
+_result_pool = _ResultPool()
 
 
 def _check_threads(threads: int) -> None:
@@ -381,7 +429,8 @@ def ktruss(graph: ZeroTerminatedCsr, k: int, options: Optional[TrussOptions] = N
     _check_threads(options.threads)
     col = _u32arr(graph.col_idx)
     cap_e = max(col.shape[0] - graph.num_vertices, 1)  # >= live edges
-    u, v, sup = _host_u32(cap_e), _host_u32(cap_e), _host_u32(cap_e)
+    owner = _result_pool.take(cap_e)
+    u, v, sup = _ResultPool.columns(owner, cap_e)
     num = _u64()
     hcap = 1 << 16
     hist = np.zeros(hcap, dtype=np.uint64)
@@ -392,7 +441,9 @@ def ktruss(graph: ZeroTerminatedCsr, k: int, options: Optional[TrussOptions] = N
                             ctypes.byref(o), _p(u), _p(v), _p(sup), cap_e,
                             ctypes.byref(num), _p(hist), hcap, ctypes.byref(it)))
     m = int(num.value)
-    return TrussResult(k, u[:m], v[:m], sup[:m], int(it.value), [int(x) for x in hist[:min(it.value, hcap)]])
+    u, v, sup = _ResultPool.finish(u, v, sup, m)
+    del owner
+    return TrussResult(k, u, v, sup, int(it.value), [int(x) for x in hist[:min(it.value, hcap)]])
 
 
 def kmax_search(graph: ZeroTerminatedCsr, options: Optional[TrussOptions] = None) -> KmaxResult:
@@ -401,7 +452,8 @@ def kmax_search(graph: ZeroTerminatedCsr, options: Optional[TrussOptions] = None
     _check_threads(options.threads)
     col = _u32arr(graph.col_idx)
     cap_e = max(col.shape[0] - graph.num_vertices, 1)
-    u, v, sup = _host_u32(cap_e), _host_u32(cap_e), _host_u32(cap_e)
+    owner = _result_pool.take(cap_e)
+    u, v, sup = _ResultPool.columns(owner, cap_e)
     num = _u64()
     hcap = 1 << 16
     hist = np.zeros(hcap, dtype=np.uint64)
@@ -413,7 +465,9 @@ def kmax_search(graph: ZeroTerminatedCsr, options: Optional[TrussOptions] = None
                                  ctypes.byref(o), ctypes.byref(kmax), _p(u), _p(v), _p(sup),
                                  cap_e, ctypes.byref(num), _p(hist), hcap, ctypes.byref(it)))
     m = int(num.value)
-    tr = TrussResult(int(kmax.value), u[:m], v[:m], sup[:m], int(it.value),
+    u, v, sup = _ResultPool.finish(u, v, sup, m)
+    del owner
+    tr = TrussResult(int(kmax.value), u, v, sup, int(it.value),
                      [int(x) for x in hist[:min(it.value, hcap)]])
     return KmaxResult(int(kmax.value), tr)
 
@@ -602,11 +656,14 @@ class Engine:
         if cap is None:  # exact survivor count (synchronises)
             self.sync()
             cap = max(1, int(self.info()["live_edges"]))
-        u, v, sup = _host_u32(cap), _host_u32(cap), _host_u32(cap)
+        owner = _result_pool.take(cap)
+        u, v, sup = _ResultPool.columns(owner, cap)
         num = _u64()
         _check(lib().ktg_engine_extract(self._h, _p(u), _p(v), _p(sup), cap, ctypes.byref(num)))
         m = int(num.value)
-        return TrussResult(0, u[:m], v[:m], sup[:m], 0, [])
+        u, v, sup = _ResultPool.finish(u, v, sup, m)
+        del owner
+        return TrussResult(0, u, v, sup, 0, [])
 
     def set_nccl(self, rank: int, world: int, unique_id: bytes) -> None:
         """Edge-partitioned fixpoint over NCCL (collective across ranks)."""
