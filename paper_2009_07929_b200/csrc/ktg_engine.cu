@@ -475,12 +475,12 @@ ktg_status build_working(ktg_engine* e, bool with_sym) {
   // edge keys in caller row order, then sort by (a, b)
   tmp = e->cub_tmp.cap;
   KTG_CUDA(cub::DeviceScan::ExclusiveSum(e->cub_tmp.p, tmp, C.deg.p, e->offs.p, (int)nb, s));
-  k_edge_keys<<<e->prune_grid, kPruneThreads, 0, s>>>(g, e->rank.p, e->offs.p, B, e->keys.p, e->vals.p,
-                                                      e->cntw.p);
+  k_edge_keys<<<e->prune_grid, kPruneThreads, 0, s>>>(g, e->rank.p, e->offs.p, B, e->keys.p, e->vals.p);
   KTG_CUDA(cudaGetLastError());
   tmp = e->cub_tmp.cap;
   KTG_CUDA(cub::DeviceRadixSort::SortPairs(e->cub_tmp.p, tmp, e->keys.p, e->keys_sorted.p, e->vals.p,
                                            e->vals_sorted.p, (int64_t)m, 0, 2 * B, s));
+  k_run_counts<<<(n + 255) / 256, 256, 0, s>>>(e->keys_sorted.p, m, n, B, e->cntw.p);
   // working row_ptr = exclusive scan of (out-degree + sentinel)
   k_row_sizes<<<4 * e->num_sms, 256, 0, s>>>(e->cntw.p, n, e->sizes.p);
   tmp = e->cub_tmp.cap;

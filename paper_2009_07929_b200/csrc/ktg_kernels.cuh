@@ -1973,8 +1973,7 @@ __global__ void k_rank_assign(const unsigned long long* __restrict__ sorted, uin
 // slot-parallel (the row of a live slot by binary search over row_ptr);
 // offs = exclusive prefix of the caller live degrees.
 __global__ void k_edge_keys(Graph g, const uint32_t* __restrict__ rank, const uint32_t* __restrict__ offs,
-                            uint32_t B, unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals,
-                            uint32_t* __restrict__ cnt) {
+                            uint32_t B, unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals) {
   for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < g.slots;
        x += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t c = g.col[x];
@@ -1992,7 +1991,28 @@ __global__ void k_edge_keys(Graph g, const uint32_t* __restrict__ rank, const ui
     const uint32_t a = min(ru, rv), b = max(ru, rv);
     keys[o] = ((unsigned long long)a << B) | b;
     vals[o] = (uint32_t)x;
-    atomicAdd(&cnt[a], 1u);
+  }
+}
+
+// Working out-degree of each rank r from the (a, b)-sorted edge keys: the
+// length of r's key run (two lower bounds), instead of one atomic per edge.
+__global__ void k_run_counts(const unsigned long long* __restrict__ keys, uint64_t m, uint32_t n, uint32_t B,
+                             uint32_t* __restrict__ cnt) {
+  for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x + 1; r <= n; r += gridDim.x * blockDim.x) {
+    uint64_t lo = 0, hi = m;
+    const unsigned long long k0 = (unsigned long long)r << B;
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (keys[mid] < k0) lo = mid + 1; else hi = mid;
+    }
+    const uint64_t first = lo;
+    hi = m;
+    const unsigned long long k1 = (unsigned long long)(r + 1) << B;
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) >> 1;
+      if (keys[mid] < k1) lo = mid + 1; else hi = mid;
+    }
+    cnt[r] = (uint32_t)(lo - first);
   }
 }
 
