@@ -475,7 +475,9 @@ ktg_status build_working(ktg_engine* e, bool with_sym) {
   // edge keys in caller row order, then sort by (a, b)
   tmp = e->cub_tmp.cap;
   KTG_CUDA(cub::DeviceScan::ExclusiveSum(e->cub_tmp.p, tmp, C.deg.p, e->offs.p, (int)nb, s));
-  k_edge_keys<<<e->prune_grid, kPruneThreads, 0, s>>>(g, e->rank.p, e->offs.p, B, e->keys.p, e->vals.p);
+  if (with_sym) KTG_TRY(sym_alloc(e, m));
+  k_edge_keys<<<e->prune_grid, kPruneThreads, 0, s>>>(g, e->rank.p, e->offs.p, B, e->keys.p, e->vals.p,
+                                                      with_sym ? e->erow.p : nullptr);
   KTG_CUDA(cudaGetLastError());
   tmp = e->cub_tmp.cap;
   KTG_CUDA(cub::DeviceRadixSort::SortPairs(e->cub_tmp.p, tmp, e->keys.p, e->keys_sorted.p, e->vals.p,
@@ -491,7 +493,6 @@ ktg_status build_working(ktg_engine* e, bool with_sym) {
     KTG_CUDA(cudaGetLastError());
     return prepare_layout(e, W, true, e->cntw.p, m);
   }
-  KTG_TRY(sym_alloc(e, m));
   unsigned long long* sz = e->sym_sizes.p;  // [tot | din | - | inoff | -] x nb
   k_sym_sizes<<<4 * e->num_sms, 256, 0, s>>>(e->symdeg_w.p, e->cntw.p, n, e->din.p, sz);
   tmp = e->cub_tmp.cap;

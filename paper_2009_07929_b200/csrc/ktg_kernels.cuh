@@ -1973,7 +1973,8 @@ __global__ void k_rank_assign(const unsigned long long* __restrict__ sorted, uin
 // slot-parallel (the row of a live slot by binary search over row_ptr);
 // offs = exclusive prefix of the caller live degrees.
 __global__ void k_edge_keys(Graph g, const uint32_t* __restrict__ rank, const uint32_t* __restrict__ offs,
-                            uint32_t B, unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals) {
+                            uint32_t B, unsigned long long* __restrict__ keys, uint32_t* __restrict__ vals,
+                            uint32_t* __restrict__ erow) {
   for (uint64_t x = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; x < g.slots;
        x += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t c = g.col[x];
@@ -1991,6 +1992,7 @@ __global__ void k_edge_keys(Graph g, const uint32_t* __restrict__ rank, const ui
     const uint32_t a = min(ru, rv), b = max(ru, rv);
     keys[o] = ((unsigned long long)a << B) | b;
     vals[o] = (uint32_t)x;
+    if (erow) erow[x] = a;  // working row of edge id x (caller order: coalesced)
   }
 }
 
@@ -2052,7 +2054,7 @@ __global__ void k_sym_sizes(const uint32_t* __restrict__ symdeg_w, const uint32_
 }
 
 // Sorted (a << B | b, caller slot) entry i of the working edges: writes the
-// working col/id, pos_of/erow of the edge id, the out-part of symmetric row
+// working col/id, pos_of of the edge id, the out-part of symmetric row
 // a, and the in-list key (b, a << 32 | working slot) of entry i (entries stay
 // in (a, b) order, so a stable sort by b alone yields ascending in-lists);
 // totals the delta queue capacity (one task per kDeltaPiece elements of
@@ -2071,8 +2073,7 @@ __global__ void k_fill_all(const unsigned long long* __restrict__ keys, const ui
     const uint32_t slot = (uint32_t)(i + a - 1);
     col_w[slot] = b;
     id_w[slot] = id;
-    y.pos_of[id] = slot;
-    const_cast<uint32_t*>(y.erow)[id] = a;
+    y.pos_of[id] = slot;  // erow[id] = a was written by k_edge_keys
     const unsigned long long dst = y.ptr[a] + din_w[a] + (slot - row_ptr_w[a]);
     y.nbr[dst] = b;
     y.eid[dst] = id;
