@@ -58,6 +58,8 @@ class _Port:
         L.orc_random_graph_raw.restype = _u64
         L.orc_support_tasks.argtypes = [_vp, _u32, _vp, _u64, _u32, _u32, _u32, _vp]
         L.orc_support_tasks.restype = _u64
+        L.orc_task_cost.argtypes = [_vp, _u32, _vp, _u64, _u32, _u64]
+        L.orc_task_cost.restype = _u64
         self.L = L
 
     def compute_supports(self, g, supports=None, threads=1):
@@ -75,6 +77,14 @@ class _Port:
         t = self.L.orc_support_tasks(_p(_u32a(g.row_ptr)), g.num_vertices, _p(_u32a(g.col_idx)),
                                      g.total_slots(), chunk, rank, world, _p(S))
         return int(t), S
+
+    def task_costs(self, g, chunk=512):
+        """Work estimate of every diagonal support task (the multi-GPU split's
+        weights, mirror of the engine's k_task_cost)."""
+        rp, col = _u32a(g.row_ptr), _u32a(g.col_idx)
+        Q = (g.total_slots() + chunk - 1) // chunk
+        return np.array([self.L.orc_task_cost(_p(rp), g.num_vertices, _p(col), g.total_slots(), chunk, q)
+                         for q in range(Q)], dtype=np.uint64)
 
     def intersect_tails(self, g, pivot, pred, S):
         return int(self.L.orc_intersect_tails(_p(_u32a(g.row_ptr)), _p(_u32a(g.col_idx)), pivot, pred, _p(S)))

@@ -292,8 +292,9 @@ uint64_t orc_random_graph_raw(uint32_t n, double p, uint64_t seed, uint64_t* out
  * k_plan_count / k_plan_write / k_support_chunked): the slot space is cut
  * into `chunk`-slot chunks; off-diagonal tasks (q, q') for the last row of
  * chunk q whose live part reaches chunk q' > q come first (q ascending, then
- * q'), then the diagonal tasks (q, q). Task t belongs to rank t % world. A
- * task processes the pivots of chunk q against the part of their a12 tails
+ * q'), then the diagonal tasks (q, q). Off-diagonal task t belongs to rank
+ * t % world; diagonal tasks are split into work-balanced contiguous chunk
+ * ranges (orc_task_cost below). A task processes the pivots of chunk q against the part of their a12 tails
  * lying in chunk q'. Diagonal tasks run from the last chunk to the first
  * (densest rows of the degree order first). This restatement computes one
  * rank's partial supports
@@ -330,6 +331,29 @@ static uint64_t merge_range(const uint32_t* row_ptr, const uint32_t* col, uint64
   return found;
 }
 
+/* Work estimate of diagonal task q (the multi-GPU split, mirror of the
+ * engine's k_task_cost): over the chunk's live pivots s, the tail inside the
+ * chunk + 1 + the live out-degree of col[s]. A chunk goes to rank
+ * min(world-1, prefix(q) * world / total): contiguous, work-balanced ranges
+ * (SURVEY.md §8(e)). */
+uint64_t orc_task_cost(const uint32_t* row_ptr, uint32_t n, const uint32_t* col, uint64_t slots, uint32_t chunk,
+                       uint64_t q) {
+  (void)n;
+  const uint64_t p0 = q * chunk, p1 = (q + 1) * chunk < slots ? (q + 1) * chunk : slots;
+  uint64_t c = 0, z = p1; /* next zero inside the chunk, scanning backwards */
+  for (uint64_t s = p1; s-- > p0;) {
+    if (col[s] == 0) {
+      z = s;
+      continue;
+    }
+    uint64_t d = 0;
+    const uint32_t v = col[s];
+    while (col[row_ptr[v] + d] != 0) ++d; /* live out-degree of v */
+    c += (z - s - 1) + 1 + d;
+  }
+  return c;
+}
+
 uint64_t orc_support_tasks(const uint32_t* row_ptr, uint32_t n, const uint32_t* col, uint64_t slots,
                            uint32_t chunk, uint32_t rank, uint32_t world, uint32_t* S) {
   const uint64_t Q = (slots + chunk - 1) / chunk;
@@ -350,13 +374,23 @@ uint64_t orc_support_tasks(const uint32_t* row_ptr, uint32_t n, const uint32_t* 
       for (uint64_t s = p_lo; s < e; ++s) tri += merge_range(row_ptr, col, s, a0, a1, S);
     }
   }
-  /* diagonal tasks, last chunk first */
-  for (uint64_t qi = 0; qi < Q; ++qi, ++t) {
-    if (t % world != rank) continue;
-    const uint64_t q = Q - 1 - qi;
+  /* diagonal tasks: this rank's work-balanced range (orc_task_cost) */
+  uint64_t* pre = (uint64_t*)malloc((Q + 1) * sizeof(uint64_t));
+  if (!pre) return 0;
+  pre[0] = 0;
+  for (uint64_t q = 0; q < Q; ++q) pre[q + 1] = pre[q] + orc_task_cost(row_ptr, n, col, slots, chunk, q);
+  const uint64_t T = pre[Q];
+  for (uint64_t q = 0; q < Q; ++q) {
+    uint64_t owner = 0;
+    if (T) {
+      owner = pre[q] * world / T;
+      if (owner > world - 1) owner = world - 1;
+    }
+    if (owner != rank) continue;
     const uint64_t p0 = q * chunk, p1 = (q + 1) * chunk < slots ? (q + 1) * chunk : slots;
     for (uint64_t s = p0; s < p1; ++s)
       if (col[s] != 0) tri += merge_range(row_ptr, col, s, s + 1, p1, S);
   }
+  free(pre);
   return tri;
 }

@@ -167,6 +167,7 @@ struct ktg_engine {
   // incremental rounds: symmetric adjacency of the working layout (+ pristine
   // copies), per-edge dead flags and positions, delta task queue
   DBuf<unsigned long long> sym_ptr, sym_sizes;
+  DBuf<unsigned long long> task_cost, task_pre;  // multi-GPU task split (per chunk)
   DBuf<uint32_t> sym_nbr, sym_eid, sym_nbr_p, sym_eid_p, sym_deg, sym_deg_p, pos_of, pos_of_p, erow, qsym,
       qrow, fq0, fq1, sym_heavy;
   DBuf<uint8_t> dead, rdirty, sdirty;
@@ -274,6 +275,8 @@ struct ktg_engine {
       b->release();
     sym_ptr.release();
     sym_sizes.release();
+    task_cost.release();
+    task_pre.release();
     dead.release();
     rdirty.release();
     sdirty.release();
@@ -791,6 +794,30 @@ ktg_status publish(ktg_engine* e) {
   return KTG_OK;
 }
 
+// Support task plan of a k_support_chunked round: off-diagonal pairs, and
+// with world > 1 this rank's work-balanced range of diagonal tasks (prefix
+// sum of per-chunk work estimates; partitioned loops are host-driven, so the
+// buffers may grow here).
+ktg_status plan_tasks(ktg_engine* e, Layout& L, const Graph& g) {
+  const cudaStream_t s = e->stream;
+  k_plan_count<<<(L.nchunks + 255) / 256, 256, 0, s>>>(g, 0);
+  k_plan_write<<<1, 1024, 0, s>>>(g);
+  if (e->world > 1) {
+    const size_t nq = (size_t)L.nchunks + 1;
+    KTG_TRY(e->task_cost.ensure(nq));
+    KTG_TRY(e->task_pre.ensure(nq));
+    size_t tmp = 0;
+    KTG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, e->task_cost.p, e->task_pre.p, (int)nq, s));
+    KTG_TRY(e->cub_tmp.ensure(tmp));
+    tmp = e->cub_tmp.cap;
+    k_task_cost<<<(unsigned)nq, kChunk, 0, s>>>(g, e->task_cost.p);
+    KTG_CUDA(cub::DeviceScan::ExclusiveSum(e->cub_tmp.p, tmp, e->task_cost.p, e->task_pre.p, (int)nq, s));
+    k_rank_range<<<1, 1, 0, s>>>(g, e->task_pre.p);
+  }
+  KTG_CUDA(cudaGetLastError());
+  return KTG_OK;
+}
+
 // Enqueue one round on the active layout:
 // plan -> support -> [check16] -> [allreduce] -> prune -> control.
 ktg_status enqueue_round(ktg_engine* e, bool graph_mode, cudaGraphConditionalHandle handle,
@@ -801,8 +828,7 @@ ktg_status enqueue_round(ktg_engine* e, bool graph_mode, cudaGraphConditionalHan
   const int fused = graph_mode ? 1 : 0;
   const bool a22 = e->inc_active && e->a22_ready && !e->a22_off_env;
   if (!a22) {
-    k_plan_count<<<(L.nchunks + 255) / 256, 256, 0, s>>>(g, 0);
-    k_plan_write<<<1, 1024, 0, s>>>(g);
+    KTG_TRY(plan_tasks(e, L, g));
   }
   if (sup0) KTG_CUDA(cudaEventRecord(sup0, s));
   if (a22) {
@@ -1065,8 +1091,7 @@ ktg_status support_pass(ktg_engine* e, int parity, uint64_t* triangles, bool max
   Graph g = e->graph_of(L);
   e->inc_active = false;
   k_begin<<<1, 1, 0, e->stream>>>(e->d_st, 0, e->opt.width_bits == 16 ? 1 : 0, parity, 0u, e->delta_ratio, e->delta_ratio0);
-  k_plan_count<<<(L.nchunks + 255) / 256, 256, 0, e->stream>>>(g, 0);
-  k_plan_write<<<1, 1024, 0, e->stream>>>(g);
+  KTG_TRY(plan_tasks(e, L, g));
   if (flag(e, KTG_FLAG_NAIVE_SUPPORT))
     k_support_naive<<<4 * e->num_sms, 256, 0, e->stream>>>(g);
   else

@@ -68,6 +68,7 @@ struct DevState {
   unsigned long long last_dcost;     //   its delta cost and keep cost
   unsigned long long last_kcost;
   double delta_ratio0;               // the same for round 0 of a run from the pristine graph
+  unsigned int dq_lo, dq_hi;         // this rank's diagonal support tasks: chunks [dq_lo, dq_hi)
 };
 
 struct Graph {
@@ -268,7 +269,72 @@ __global__ void __launch_bounds__(1024) k_plan_write(Graph g) {
   if (tid == blockDim.x - 1) {
     g.st->npairs = off;
     g.st->task_next = 0;
+    g.st->dq_lo = 0;  // one rank: every diagonal task (k_rank_range narrows it)
+    g.st->dq_hi = Q;
   }
+}
+
+// Multi-GPU work-balanced split: estimated work of diagonal
+// task q = sum over its live pivots s of (tail inside the chunk + 1 +
+// live out-degree of col[s]); CTA per chunk, next zeros from a backward
+// scan of the staged chunk. cost[Q] = 0 so an exclusive scan ends in the
+// total. oracle/ktruss_oracle.c:orc_task_cost restates it.
+__global__ void __launch_bounds__(kChunk) k_task_cost(Graph g, unsigned long long* __restrict__ cost) {
+  __shared__ uint32_t nz[kChunk];
+  __shared__ unsigned long long red[kChunk / 32];
+  const uint32_t q = blockIdx.x, x = threadIdx.x;
+  if (q >= g.nchunks) {
+    if (q == g.nchunks && x == 0) cost[q] = 0;
+    return;
+  }
+  const uint64_t p0 = (uint64_t)q * kChunk;
+  const uint32_t plen = (uint32_t)umin64(kChunk, g.slots - p0);
+  const uint32_t v = x < plen ? g.col[p0 + x] : 0u;
+  nz[x] = (x < plen && v != 0) ? kChunk : x;  // zero (or past the end): its own index
+  __syncthreads();
+  // next zero at or after x: suffix minimum (Hillis-Steele, log2(kChunk) steps)
+  for (uint32_t o = 1; o < kChunk; o <<= 1) {
+    const uint32_t y = x + o < kChunk ? nz[x + o] : (uint32_t)kChunk;
+    __syncthreads();
+    nz[x] = min(nz[x], y);
+    __syncthreads();
+  }
+  unsigned long long c = 0;
+  if (x < plen && v != 0) c = (unsigned long long)(min(nz[x], plen) - x - 1) + 1ull + g.deg[v];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((x & 31) == 0) red[x >> 5] = c;
+  __syncthreads();
+  if (x == 0) {
+    unsigned long long t = 0;
+    for (int w = 0; w < kChunk / 32; ++w) t += red[w];
+    cost[q] = t;
+  }
+}
+
+// This rank's diagonal chunks: chunk q goes to rank min(world-1,
+// pre[q] * world / total) (pre = exclusive prefix of the task costs), which
+// is non-decreasing in q, so every rank owns one contiguous range.
+__global__ void k_rank_range(Graph g, const unsigned long long* __restrict__ pre) {
+  const uint32_t Q = g.nchunks;
+  const unsigned long long T = pre[Q];
+  auto owner = [&](uint32_t q) -> uint32_t {
+    if (T == 0) return 0u;
+    const unsigned long long r = pre[q] * g.world / T;
+    return (uint32_t)(r < g.world - 1 ? r : g.world - 1);
+  };
+  auto first = [&](uint32_t r) -> uint32_t {  // first q with owner(q) >= r
+    if (r == 0) return 0u;
+    if (r >= g.world) return Q;
+    uint32_t lo = 0, hi = Q;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (owner(mid) < r) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+  };
+  g.st->dq_lo = first(g.rank);
+  g.st->dq_hi = first(g.rank + 1);
 }
 
 // ---------------------------------------------------------------------------
@@ -448,8 +514,12 @@ k_support_chunked(Graph g) {
   if (g.st->mode) return;  // supports carried this round (incremental mode)
   uint32_t* __restrict__ S = cur_S(g);
   const uint32_t* __restrict__ col = g.col;
+  // this rank's tasks: off-diagonal pairs t = l * world + rank, then its
+  // diagonal chunk range [dq_lo, dq_hi) densest (highest) first
   const uint32_t npairs = g.st->npairs;
-  const uint32_t ntasks = npairs + g.nchunks;
+  const uint32_t noff = npairs > g.rank ? (npairs - g.rank + g.world - 1) / g.world : 0u;
+  const uint32_t dq_lo = g.st->dq_lo, dq_hi = g.st->dq_hi;
+  const uint32_t ntasks = noff + (dq_hi - dq_lo);
   const uint32_t ratio = g.scan_ratio;
   const uint32_t h0 = g.st->h0;  // pivots (i, j) with j < h0 cannot matter (see k_heavy_rank)
   const unsigned lt_mask = (1u << lane) - 1u;
@@ -470,16 +540,14 @@ k_support_chunked(Graph g) {
     }
     __syncthreads();
     const uint32_t local = s.task;
-    const uint64_t t64 = (uint64_t)local * g.world + g.rank;
-    if (t64 >= ntasks) break;
-    const uint32_t t = (uint32_t)t64;
+    if (local >= ntasks) break;
     uint32_t q, q2;
-    if (t < npairs) {
-      const uint2 pr = g.pairs[t];
+    if (local < noff) {
+      const uint2 pr = g.pairs[local * g.world + g.rank];
       q = pr.x;
       q2 = pr.y;
     } else {
-      q = q2 = g.nchunks - 1 - (t - npairs);  // dense (high-rank) chunks first
+      q = q2 = dq_hi - 1 - (local - noff);  // dense (high-rank) chunks first
     }
     const bool diag = q == q2;
     const uint64_t a0 = (uint64_t)q2 * kChunk;

@@ -119,3 +119,22 @@ def test_partitioned_fixpoint_equals_single_process():
         for r in (r0, r1):
             assert r[k][2] == hist
             assert np.array_equal(r[k][0], col) and np.array_equal(r[k][1], S)
+
+
+def test_task_split_is_work_balanced():
+    """the diagonal support tasks are split into contiguous
+    chunk ranges of equal estimated work (prefix sum of the per-chunk work,
+    mirror of k_task_cost / k_rank_range); equal slot counts are not."""
+    import oracle
+    from paper_2009_07929_b200 import graph
+    g = graph.rmat(14, 16, 42)
+    c = oracle.port().task_costs(g).astype(np.float64)
+    T, Q = c.sum(), len(c)
+    pre = np.concatenate([[0.0], np.cumsum(c)])
+    for w in (2, 4, 8):
+        own = np.minimum(w - 1, (pre[:-1] * w // T)).astype(int)
+        assert np.all(np.diff(own) >= 0)  # contiguous ranges
+        tot = np.bincount(own, weights=c, minlength=w)
+        assert tot.max() / tot.mean() < 1.02, w
+        eq = np.bincount(np.minimum(w - 1, np.arange(Q) * w // Q), weights=c, minlength=w)
+        assert eq.max() / eq.mean() > 1.2, w
