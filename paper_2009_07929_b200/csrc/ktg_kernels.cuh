@@ -1365,58 +1365,80 @@ __device__ __forceinline__ uint32_t mark_removed(const Graph& g, const Sym& y, u
   return min(y.deg[u], y.deg[v]);
 }
 
-// Mode 0: warp per row, every live edge; S < k-2 is removed (truss.cpp:31).
-// Totals removed, sum S (3T of G_r), delta cost and keep cost.
+// Mode 0: thread per slot, every live edge (row of a slot by a binary search
+// among the rows of its chunk; working rows are short in degree order, so a
+// warp per row would idle most lanes); S < k-2 is removed (truss.cpp:31).
+// Removed edge ids are queued on this round's frontier list (empty after a
+// full pass), block-aggregated, for k_delta. Totals removed, sum S (3T of
+// G_r), delta cost and keep cost.
 __global__ void __launch_bounds__(kPruneThreads)
 k_mark(Graph g, Sym y) {
   if (g.st->mode != 0) return;
-  const int lane = threadIdx.x & 31;
-  const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
-  const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+  __shared__ uint32_t wcnt[kPruneThreads / 32];
+  __shared__ uint32_t qbase;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const uint32_t* __restrict__ S = cur_S(g);
   const uint32_t thr = g.st->threshold;
   const uint32_t h0 = g.st->h0;
+  const uint32_t fpar = g.st->fpar;
+  uint32_t* __restrict__ fq = fpar ? y.fq1 : y.fq0;
   unsigned long long removed = 0, sum_s = 0, dcost = 0, kcost = 0;
-  for (uint32_t u = warp + 1; u <= g.n; u += nwarps) {
-    const uint32_t d = g.deg[u];
-    if (d == 0) continue;
-    const uint32_t base = g.row_ptr[u];
-    for (uint32_t off = 0; off < d; off += 32) {
-      const uint32_t idx = off + lane;
-      const uint32_t p = base + idx;
-      bool rm = false;
-      if (idx < d) {
-        const uint32_t v = g.col[p];
-        const uint32_t sv = u < h0 ? 0u : S[p];  // rows below h0 go whatever their count
-        sum_s += sv;
-        if (sv < thr || u < h0) {
-          rm = true;
-          dcost += mark_removed<true>(g, y, p, u, v, g.payload[p]);
-        } else {
-          kcost += min(y.deg[u], y.deg[v]);
-        }
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t b0 = (uint64_t)blockIdx.x * blockDim.x; b0 < g.slots; b0 += stride) {
+    const uint64_t p = b0 + threadIdx.x;
+    bool rm = false;
+    uint32_t id = 0;
+    const uint32_t v = p < g.slots ? g.col[p] : 0u;
+    if (v != 0) {
+      const uint32_t q = (uint32_t)(p / kChunk);
+      uint32_t lo = q ? g.chunk_row[q - 1] : 0u, hi = g.chunk_row[q] + 1;
+      while (lo < hi) {  // row u = upper_bound(row_ptr, p) - 1
+        const uint32_t mid = (lo + hi) >> 1;
+        if (g.row_ptr[mid] <= (uint32_t)p) lo = mid + 1; else hi = mid;
       }
-      const unsigned rmask = __ballot_sync(0xffffffffu, rm);
-      if (rmask && lane == 0) {
-        y.rdirty[u] = 1;
-        y.sdirty[u] = 1;
-        removed += __popc(rmask);
+      const uint32_t u = lo - 1;
+      const uint32_t sv = u < h0 ? 0u : S[p];  // rows below h0 go whatever their count
+      sum_s += sv;
+      if (sv < thr || u < h0) {
+        rm = true;
+        id = g.payload[p];
+        dcost += mark_removed<true>(g, y, (uint32_t)p, u, v, id);
+        if (!y.rdirty[u]) y.rdirty[u] = 1;
+        if (!y.sdirty[u]) y.sdirty[u] = 1;
+      } else {
+        kcost += min(y.deg[u], y.deg[v]);
       }
     }
+    // block-aggregated append of the removed ids to the frontier list
+    const unsigned m = __ballot_sync(0xffffffffu, rm);
+    if (lane == 0) wcnt[wid] = __popc(m);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      uint32_t t = 0;
+      for (int w = 0; w < kPruneThreads / 32; ++w) {
+        const uint32_t c = wcnt[w];
+        wcnt[w] = t;
+        t += c;
+      }
+      qbase = t ? atomicAdd(&g.st->nfq[fpar], t) : 0u;
+      removed += t;
+    }
+    __syncthreads();
+    if (rm) fq[qbase + wcnt[wid] + __popc(m & ((1u << lane) - 1u))] = id;
+    __syncthreads();
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
-    removed += __shfl_xor_sync(0xffffffffu, removed, o);
     sum_s += __shfl_xor_sync(0xffffffffu, sum_s, o);
     dcost += __shfl_xor_sync(0xffffffffu, dcost, o);
     kcost += __shfl_xor_sync(0xffffffffu, kcost, o);
   }
   if (lane == 0) {
-    if (removed) atomicAdd(&g.st->removed, removed);
     if (sum_s) atomicAdd(&g.st->sum_s, sum_s);
     if (dcost) atomicAdd(&g.st->delta_cost, dcost);
     if (kcost) atomicAdd(&g.st->keep_cost, kcost);
   }
+  if (threadIdx.x == 0 && removed) atomicAdd(&g.st->removed, removed);
 }
 
 // Mode 1: thread per frontier edge (queued by the previous round's k_delta).
@@ -1582,23 +1604,7 @@ k_delta(Graph g, Sym y) {
       for (uint32_t t = 0; t < np; ++t) y.rq[at + t] = make_uint4(p, u, v, t);
     }
   };
-  if (g.st->mode == 0) {
-    for (uint32_t u = warp + 1; u <= g.n; u += nwarps) {
-      const uint32_t d = g.deg[u];
-      if (d == 0) continue;
-      const uint32_t base = g.row_ptr[u];
-      for (uint32_t off = 0; off < d; off += 32) {
-        const uint32_t c = off + lane < d ? g.col[base + off + lane] : 0u;
-        unsigned m = __ballot_sync(0xffffffffu, c & kDeadMark);
-        while (m) {
-          const int b = __ffs(m) - 1;
-          m &= m - 1;
-          const uint32_t v = __shfl_sync(0xffffffffu, c, b) & ~kDeadMark;
-          edge(base + off + b, u, v);
-        }
-      }
-    }
-  } else {
+  {  // the removal set: queued by k_mark (mode 0) or by the last k_delta (mode 1)
     const uint32_t fpar = g.st->fpar;
     const uint32_t nf = g.st->nfq[fpar];
     const uint32_t* __restrict__ fq = fpar ? y.fq1 : y.fq0;
