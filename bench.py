@@ -14,7 +14,7 @@ edges (bench.cpp:45); time-to-fixpoint per K is reported alongside.
   e2e      the same sweep through the reference-shaped C ABI with HOST
            buffers (ktg_ktruss: H2D of the CSR, fixpoint, D2H of the truss)
            per K, from pinned memory.
-  roofline the support kernel (k_support_chunked): algorithmic bytes of
+  roofline the support kernel (k_support_a22): algorithmic bytes of
            SURVEY.md §8(d) per launch / its CUDA-event duration (host-driven
            instrumented pass, sampled K values).
   cpu_baseline  the reference library itself (oracle/_ref, Strategy::Fine,

@@ -37,6 +37,19 @@ e.reset(); h = e.run(km)
 print(f"K_max fixpoint: rounds={len(h)} ms={e.info()['device_ms']:.1f}", flush=True)
 out.update({"kmax": km, "kmax_rounds": len(h), "kmax_ms": e.info()["device_ms"], "kmax_survivors": e.info()["live_edges"]})
 e.close()
+# the default path's support kernel (k_support_a22, carried supports) on its
+# full passes, without the round-0 degree bound so round 0 is a whole pass
+ew = kt.Engine(g, kt.TrussOptions(no_degree_bound=True), collect_work=True)
+et = kt.Engine(g, kt.TrussOptions(no_degree_bound=True), time_support=True)
+for k in (3, km):
+    ew.reset(); ew.run(k); w = ew.round_work(); et.reset(); et.run(k); tw = et.round_work()
+    full = [(x, t) for x, t in zip(w, tw) if t["full_pass"]]
+    B = sum(4*x["L"] + 4*g.total_slots() + 4*(g.num_vertices+2) + 12*x["triangles"] for x, _ in full)
+    T = sum(t["support_ms"] for _, t in full)
+    print(f"K={k} a22 full passes: {len(full)} ms={T:.1f} bytes={B/1e9:.1f}GB -> {B/T/1e6:.0f} GB/s", flush=True)
+    out[f"k{k}_a22_GBps"] = B / T / 1e6
+    out[f"k{k}_a22_ms"] = T
+ew.close(); et.close()
 ew = kt.Engine(g, kt.TrussOptions(recompute=True), collect_work=True)
 et = kt.Engine(g, kt.TrussOptions(recompute=True), time_support=True)
 for k in (3, km):
