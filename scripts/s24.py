@@ -10,6 +10,24 @@ scale = int(sys.argv[1]) if len(sys.argv) > 1 else 24
 t = time.time()
 g = kt.rmat(scale)
 print(f"gen s{scale}: {time.time()-t:.1f}s n={g.num_vertices} m={g.num_edges} slots={g.total_slots()}", flush=True)
+if "--a22" in sys.argv:
+    # the default path's support kernel (k_support_a22, carried supports) on
+    # its full passes, without the round-0 degree bound so round 0 is a
+    # whole pass; one engine records both the work and the kernel times
+    ea = kt.Engine(g, kt.TrussOptions(no_degree_bound=True), collect_work=True, time_support=True)
+    res = {}
+    for k in (3, 10, 100, 935):
+        ea.reset(); ea.run(k); w = ea.round_work()
+        full = [x for x in w if x["full_pass"]]
+        B = sum(4*x["L"] + 4*g.total_slots() + 4*(g.num_vertices+2) + 12*x["triangles"] for x in full)
+        X = sum(4*x["L_tail"] + 4*g.total_slots() + 8*x["live_edges"] + 8*(g.num_vertices+2) + 12*x["triangles"]
+                for x in full)
+        T = sum(x["support_ms"] for x in full)
+        print(f"K={k} a22 full passes: {len(full)} ms={T:.1f} algorithmic={B/1e9:.0f}GB -> {B/T/1e6:.0f} GB/s; "
+              f"executed={X/1e9:.0f}GB -> {X/T/1e6:.0f} GB/s", flush=True)
+        res[k] = {"full_passes": len(full), "ms": T, "alg_GBps": B / T / 1e6, "exec_GBps": X / T / 1e6}
+    json.dump(res, open(f"gpurun_out/s{scale}_a22.json", "w"), indent=1)
+    sys.exit(0)
 t = time.time()
 e = kt.Engine(g)
 print(f"load+reorient: {time.time()-t:.1f}s", flush=True)
@@ -37,19 +55,6 @@ e.reset(); h = e.run(km)
 print(f"K_max fixpoint: rounds={len(h)} ms={e.info()['device_ms']:.1f}", flush=True)
 out.update({"kmax": km, "kmax_rounds": len(h), "kmax_ms": e.info()["device_ms"], "kmax_survivors": e.info()["live_edges"]})
 e.close()
-# the default path's support kernel (k_support_a22, carried supports) on its
-# full passes, without the round-0 degree bound so round 0 is a whole pass
-ew = kt.Engine(g, kt.TrussOptions(no_degree_bound=True), collect_work=True)
-et = kt.Engine(g, kt.TrussOptions(no_degree_bound=True), time_support=True)
-for k in (3, km):
-    ew.reset(); ew.run(k); w = ew.round_work(); et.reset(); et.run(k); tw = et.round_work()
-    full = [(x, t) for x, t in zip(w, tw) if t["full_pass"]]
-    B = sum(4*x["L"] + 4*g.total_slots() + 4*(g.num_vertices+2) + 12*x["triangles"] for x, _ in full)
-    T = sum(t["support_ms"] for _, t in full)
-    print(f"K={k} a22 full passes: {len(full)} ms={T:.1f} bytes={B/1e9:.1f}GB -> {B/T/1e6:.0f} GB/s", flush=True)
-    out[f"k{k}_a22_GBps"] = B / T / 1e6
-    out[f"k{k}_a22_ms"] = T
-ew.close(); et.close()
 ew = kt.Engine(g, kt.TrussOptions(recompute=True), collect_work=True)
 et = kt.Engine(g, kt.TrussOptions(recompute=True), time_support=True)
 for k in (3, km):

@@ -59,3 +59,22 @@ def test_engine_reload_sizes(port):
             col, S = e.read()
             col_e, S_e, hist_e = port.run_fixpoint(g, k, threads=4)
             assert hist == hist_e and np.array_equal(col, col_e) and np.array_equal(S, S_e), (scale, k)
+
+
+def test_results_survive_later_calls(port):
+    """ktruss results live in pooled page-locked buffers: a result kept by the
+    caller must not be overwritten by later calls (large results stay views
+    of their buffer, small ones are copied out)."""
+    g = kt.rmat(16, 16, seed=42)  # K=3/4 results exceed the copy-out size
+    kept = {k: kt.ktruss(g, k) for k in (3, 4, 60)}
+    assert kept[3].u.base is not None  # a view of a pooled buffer
+    for _ in range(3):  # churn the pool with other K values
+        for k in (5, 30, 3):
+            kt.ktruss(g, k)
+    for k, r in kept.items():
+        e, hist = port.truss_edges(g, k, threads=4)
+        assert np.array_equal(r.edges, e) and r.removed_per_iteration == hist, k
+    del kept
+    r = kt.ktruss(g, 3)  # buffers released above are reused
+    e, _ = port.truss_edges(g, 3, threads=4)
+    assert np.array_equal(r.edges, e)
