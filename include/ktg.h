@@ -267,6 +267,30 @@ ktg_status ktg_engine_set_partition(ktg_engine* e, uint32_t rank, uint32_t world
 ktg_status ktg_nccl_unique_id(uint8_t* out_128_bytes);
 ktg_status ktg_engine_set_nccl(ktg_engine* e, uint32_t rank, uint32_t world, const uint8_t* unique_id);
 
+/* Fused multi-GPU support pass (reduce-scatter fused into the
+ * support kernel): the support buffers are split into `world` contiguous
+ * owned spans (span = ceil(slots / world) slots); rank r's k_support_chunked
+ * sends every increment straight to the owner's buffer with atomics on
+ * NVLink peer memory, so no separate reduce step runs. peer_s0/peer_s1 hold
+ * every rank's support buffers (ktg_engine_support_buffers on each rank,
+ * mapped into this process: cudaIpcOpenMemHandle across processes, or plain
+ * pointers for ranks sharing a process/device); entry `rank` must be this
+ * engine's own. The exchange callback runs on the calling thread of the
+ * host-driven loop: phase 0 before each support pass (wait for the stream,
+ * then for every rank: each rank's previous prune zeroed the buffer the
+ * others now add into), phase 1 after it (wait for the stream and every
+ * rank, copy every other rank's owned span of the current buffer into
+ * d_supports, replace *d_triangles (device u64) by the sum over ranks, and
+ * wait again before returning). Call after loading the graph. */
+typedef int (*ktg_peer_cb)(int phase, uint32_t* d_supports, uint64_t slots, uint64_t span,
+                           unsigned long long* d_triangles, void* stream, void* user);
+ktg_status ktg_engine_support_buffers(ktg_engine* e, uint32_t** d_s0, uint32_t** d_s1, uint64_t* slots);
+ktg_status ktg_engine_set_peers(ktg_engine* e, uint32_t rank, uint32_t world, uint32_t* const* peer_s0,
+                                uint32_t* const* peer_s1, ktg_peer_cb cb, void* user);
+/* cudaMemcpyAsync(cudaMemcpyDefault) + stream synchronize: a helper for
+ * exchange callbacks written in a host language without CUDA bindings. */
+ktg_status ktg_device_copy(void* dst, const void* src, uint64_t bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -206,6 +206,13 @@ struct ktg_engine {
   uint32_t scan_ratio = kScanRatio;
   ktg_allreduce_cb allreduce = nullptr;
   void* allreduce_user = nullptr;
+  // fused reduce-scatter (ktg_engine_set_peers): [S0 of every rank | S1 of
+  // every rank] as device pointers, the owned span, the exchange callback
+  DBuf<uint32_t*> peer_tab;
+  uint32_t npeer = 0;
+  uint64_t peer_span = 0;
+  ktg_peer_cb peer_cb = nullptr;
+  void* peer_user = nullptr;
   ncclComm_t nccl = nullptr;
 
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evs0 = nullptr, evs1 = nullptr;
@@ -234,6 +241,10 @@ struct ktg_engine {
     g.world = world;
     g.scan_ratio = scan_ratio;
     g.payload = L.has_payload ? L.id.p : nullptr;
+    g.peer0 = npeer ? peer_tab.p : nullptr;
+    g.peer1 = npeer ? peer_tab.p + npeer : nullptr;
+    g.span = peer_span;
+    g.npeer = npeer;
     return g;
   }
 
@@ -277,6 +288,7 @@ struct ktg_engine {
     sym_sizes.release();
     task_cost.release();
     task_pre.release();
+    peer_tab.release();
     dead.release();
     rdirty.release();
     sdirty.release();
@@ -837,6 +849,11 @@ ktg_status enqueue_round(ktg_engine* e, bool graph_mode, cudaGraphConditionalHan
   } else if (flag(e, KTG_FLAG_NAIVE_SUPPORT)) {
     k_support_naive<<<4 * e->num_sms, 256, 0, s>>>(g);
   } else {
+    const bool exch = !graph_mode && e->npeer > 1 && e->peer_cb;
+    // fused path: every rank's previous prune (which zeroes this round's
+    // buffer) must be done before any rank adds into it
+    if (exch && e->peer_cb(0, nullptr, L.slots, e->peer_span, nullptr, s, e->peer_user) != 0)
+      return fail(KTG_ERR_CUDA, "peer exchange callback failed (round start)");
     k_support_chunked<<<e->support_grid, kSupportThreads, e->support_smem, s>>>(g);
   }
   if (sup1) KTG_CUDA(cudaEventRecord(sup1, s));
@@ -861,7 +878,14 @@ ktg_status enqueue_round(ktg_engine* e, bool graph_mode, cudaGraphConditionalHan
   }
   if (e->opt.width_bits == 16) k_check16<<<4 * e->num_sms, 256, 0, s>>>(g);
   KTG_CUDA(cudaGetLastError());
-  if (!graph_mode && (e->nccl || (e->world > 1 && e->allreduce))) {
+  if (!graph_mode && e->npeer > 1 && e->peer_cb) {
+    // fused path: the support kernel already sent every increment to its
+    // owner; the callback waits for all ranks, all-gathers the owned spans
+    // and sums the round's triangle count
+    uint32_t* buf = e->h_st->parity ? L.S1.p : L.S0.p;
+    if (e->peer_cb(1, buf, L.slots, e->peer_span, &e->d_st->triangles, s, e->peer_user) != 0)
+      return fail(KTG_ERR_CUDA, "peer exchange callback failed (all-gather)");
+  } else if (!graph_mode && (e->nccl || (e->world > 1 && e->allreduce))) {
     // partial supports of this rank's task share -> full supports everywhere
     uint32_t* buf = e->h_st->parity ? L.S1.p : L.S0.p;
     if (e->nccl) {
@@ -1480,6 +1504,51 @@ ktg_status ktg_nccl_unique_id(uint8_t* out) {
   const ncclResult_t r = api->getUniqueId(&id);
   if (r != ncclSuccess) return fail(KTG_ERR_CUDA, std::string("ncclGetUniqueId: ") + api->errorString(r));
   std::memcpy(out, &id, sizeof(id));
+  return KTG_OK;
+}
+
+ktg_status ktg_engine_support_buffers(ktg_engine* e, uint32_t** s0, uint32_t** s1, uint64_t* slots) {
+  Layout& L = e->act();
+  if (!L.ready) return fail(KTG_ERR_INVALID_PARAMETER, "engine has no graph loaded");
+  if (s0) *s0 = L.S0.p;
+  if (s1) *s1 = L.S1.p;
+  if (slots) *slots = L.slots;
+  return KTG_OK;
+}
+
+ktg_status ktg_engine_set_peers(ktg_engine* e, uint32_t rank, uint32_t world, uint32_t* const* peer_s0,
+                                uint32_t* const* peer_s1, ktg_peer_cb cb, void* user) {
+  if (world == 0 || rank >= world) return fail(KTG_ERR_INVALID_PARAMETER, "rank must be < world");
+  Layout& L = e->act();
+  if (!L.ready) return fail(KTG_ERR_INVALID_PARAMETER, "load the graph before ktg_engine_set_peers");
+  if (world > 1 && (!peer_s0 || !peer_s1 || !cb))
+    return fail(KTG_ERR_INVALID_PARAMETER, "world > 1 needs peer buffers and an exchange callback");
+  if (world > 1 && (peer_s0[rank] != L.S0.p || peer_s1[rank] != L.S1.p))
+    return fail(KTG_ERR_INVALID_PARAMETER, "peer tables must hold this engine's own support buffers at its rank");
+  e->rank_id = rank;
+  e->world = world;
+  e->allreduce = nullptr;
+  e->npeer = world > 1 ? world : 0;
+  e->peer_span = (L.slots + world - 1) / world;
+  e->peer_cb = cb;
+  e->peer_user = user;
+  if (world > 1) {
+    std::vector<uint32_t*> tab(2 * (size_t)world);
+    for (uint32_t r = 0; r < world; ++r) {
+      tab[r] = peer_s0[r];
+      tab[world + r] = peer_s1[r];
+    }
+    KTG_TRY(e->peer_tab.ensure(tab.size()));
+    KTG_CUDA(cudaMemcpy(e->peer_tab.p, tab.data(), tab.size() * sizeof(uint32_t*), cudaMemcpyHostToDevice));
+  }
+  if (e->exec) cudaGraphExecDestroy(e->exec);
+  e->exec = nullptr;
+  return KTG_OK;
+}
+
+ktg_status ktg_device_copy(void* dst, const void* src, uint64_t bytes, void* stream) {
+  KTG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, (cudaStream_t)stream));
+  KTG_CUDA(cudaStreamSynchronize((cudaStream_t)stream));
   return KTG_OK;
 }
 

@@ -90,7 +90,25 @@ struct Graph {
   uint32_t world;
   uint32_t scan_ratio;      // SCAN N+(j) when |N+(j)| <= ratio * |tail|
   uint32_t* payload;        // per-slot id compacted along with col (working layout) or null
+  // fused reduce-scatter (multi-GPU, ktg_engine_set_peers): every support
+  // increment goes straight to the owner rank's buffer (slot / span) over
+  // NVLink peer memory; npeer = 0 keeps local increments
+  uint32_t* const* peer0;   // per rank: its S0 (device pointers, peer-mapped)
+  uint32_t* const* peer1;   // per rank: its S1
+  uint64_t span;            // slots owned per rank
+  uint32_t npeer;
 };
+
+// One support increment: local buffer, or the owning rank's buffer when the
+// support pass is fused with the reduce-scatter.
+__device__ __forceinline__ void sadd(const Graph& g, uint32_t* __restrict__ S, uint64_t slot, uint32_t v) {
+  if (g.npeer == 0) {
+    atomicAdd(S + slot, v);
+    return;
+  }
+  uint32_t* const* tab = g.st->parity ? g.peer1 : g.peer0;
+  atomicAdd(tab[(uint32_t)(slot / g.span)] + slot, v);
+}
 
 // Symmetric adjacency of the working layout for incremental rounds: row v
 // lists every live neighbour of v (in-neighbours then out-neighbours, so the
@@ -466,7 +484,8 @@ __device__ __forceinline__ uint32_t block_exscan(uint32_t v, uint32_t* red, uint
 // Confirms one queued filter positive: binary search of k in the pivot's
 // tail; on a match bumps the tail slot (smem), the A22 slot (global) and the
 // pivot count (smem).
-__device__ __forceinline__ bool confirm(SupportSmem& s, uint32_t* __restrict__ S, uint32_t* cntPiv, bool diag,
+__device__ __forceinline__ bool confirm(const Graph& g, SupportSmem& s, uint32_t* __restrict__ S, uint32_t* cntPiv,
+                                        bool diag,
                                         uint32_t k, uint32_t pos, uint32_t p) {
   const uint32_t te = s.te[p] & 0x7fffu;
   const uint32_t tb = diag ? p + 1 : 0;
@@ -479,7 +498,7 @@ __device__ __forceinline__ bool confirm(SupportSmem& s, uint32_t* __restrict__ S
   }
   if (x < (uint32_t)kChunk) {
     atomicAdd(&s.cntA[x], 1u);
-    atomicAdd(&S[pos], 1u);
+    sadd(g, S, pos, 1u);
     atomicAdd(&cntPiv[p], 1u);
     return true;
   }
@@ -719,7 +738,7 @@ k_support_chunked(Graph g) {
             const uint32_t y = lb_global(col, db0, db1, kk);
             if (y < db1 && __ldg(col + y) == kk) {
               atomicAdd(&s.cntA[x], 1u);
-              atomicAdd(&S[y], 1u);
+              sadd(g, S, y, 1u);
               atomicAdd(&cntPiv[p], 1u);
               ++tri_local;
             }
@@ -736,14 +755,14 @@ k_support_chunked(Graph g) {
         if (qn >= 32) {
           __syncwarp();
           const uint32_t e = qn - 32 + lane;
-          tri_local += confirm(s, S, cntPiv, diag, qk[e], qpos[e], qp[e]);
+          tri_local += confirm(g, s, S, cntPiv, diag, qk[e], qpos[e], qp[e]);
           qn -= 32;
           __syncwarp();
         }
       }
     }
     __syncwarp();
-    if (lane < qn) tri_local += confirm(s, S, cntPiv, diag, qk[lane], qpos[lane], qp[lane]);
+    if (lane < qn) tri_local += confirm(g, s, S, cntPiv, diag, qk[lane], qpos[lane], qp[lane]);
     __syncthreads();
 
     // 4. flush smem counts
@@ -751,10 +770,10 @@ k_support_chunked(Graph g) {
     for (int e = 0; e < EPT; ++e) {
       const uint32_t x = tid * EPT + e;
       const uint32_t ca = s.cntA[x];
-      if (ca) atomicAdd(&S[a0 + x], ca);
+      if (ca) sadd(g, S, a0 + x, ca);
       if (!diag) {
         const uint32_t cp = s.cntP[x];
-        if (cp) atomicAdd(&S[p0 + x], cp);
+        if (cp) sadd(g, S, p0 + x, cp);
       }
     }
     __syncthreads();

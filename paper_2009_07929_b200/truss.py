@@ -136,6 +136,8 @@ class KmaxResult:
 # ---------------------------------------------------------------------------
 ROUND_CB = ctypes.CFUNCTYPE(None, ctypes.POINTER(_u32), ctypes.POINTER(_u32), _u64, _u64, _vp)
 ALLREDUCE_CB = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.POINTER(_u32), _u64, _vp, _vp)
+# ktg_peer_cb(phase, d_supports, slots, span, d_triangles, stream, user)
+PEER_CB = ctypes.CFUNCTYPE(ctypes.c_int, ctypes.c_int, _vp, _u64, _u64, _vp, _vp, _vp)
 
 
 class _Options(ctypes.Structure):
@@ -207,6 +209,9 @@ def lib():
         L.ktg_engine_device_state.argtypes = [_vp, P(_vp), P(_vp), P(_vp)]
         L.ktg_engine_extract.argtypes = [_vp, _vp, _vp, _vp, _u64, P(_u64)]
         L.ktg_engine_set_partition.argtypes = [_vp, _u32, _u32, ALLREDUCE_CB, _vp]
+        L.ktg_engine_support_buffers.argtypes = [_vp, P(_vp), P(_vp), P(_u64)]
+        L.ktg_engine_set_peers.argtypes = [_vp, _u32, _u32, _vp, _vp, PEER_CB, _vp]
+        L.ktg_device_copy.argtypes = [_vp, _vp, _u64, _vp]
         L.ktg_nccl_unique_id.argtypes = [_vp]
         L.ktg_engine_set_nccl.argtypes = [_vp, _u32, _u32, _vp]
         _configured = True
@@ -480,6 +485,12 @@ class detail:  # namespace ktruss::detail (truss.hpp:58-63)
 # Device-resident engine (what the benchmark times)
 # ---------------------------------------------------------------------------
 
+def device_copy(dst: int, src: int, nbytes: int, stream: Optional[int] = None) -> None:
+    """cudaMemcpyAsync(cudaMemcpyDefault) + synchronize (device or host
+    pointers), for peer-exchange callbacks."""
+    _check(lib().ktg_device_copy(dst, src, nbytes, stream))
+
+
 def nccl_unique_id() -> bytes:
     """ncclGetUniqueId (128 bytes) for Engine.set_nccl."""
     buf = (ctypes.c_uint8 * 128)()
@@ -669,6 +680,34 @@ class Engine:
         """Edge-partitioned fixpoint over NCCL (collective across ranks)."""
         buf = (ctypes.c_uint8 * 128).from_buffer_copy(unique_id)
         _check(lib().ktg_engine_set_nccl(self._h, rank, world, buf))
+
+    def support_buffers(self):
+        """Device pointers of the active layout's two support buffers and
+        the slot count (what peers add into under set_peers)."""
+        a, b, n = _vp(), _vp(), _u64()
+        _check(lib().ktg_engine_support_buffers(self._h, ctypes.byref(a), ctypes.byref(b), ctypes.byref(n)))
+        return a.value, b.value, int(n.value)
+
+    def set_peers(self, rank: int, world: int, s0, s1, exchange) -> None:
+        """Fused multi-GPU support pass: increments go straight to the owner
+        rank's buffer (peer pointers s0/s1, one per rank, this engine's own at
+        `rank`); `exchange(phase, d_supports, slots, span, d_triangles,
+        stream)` is the ktg_peer_cb contract of include/ktg.h."""
+        t0 = (ctypes.c_void_p * world)(*s0)
+        t1 = (ctypes.c_void_p * world)(*s1)
+
+        def tramp(phase, d_s, slots, span, d_tri, stream, user):
+            try:
+                exchange(int(phase), d_s, int(slots), int(span), d_tri, stream)
+                return 0
+            except Exception:  # surfaces as KTG_ERR_CUDA
+                import traceback
+                traceback.print_exc()
+                return 1
+
+        cb = PEER_CB(tramp)
+        self._keep["peers"] = (t0, t1, cb)
+        _check(lib().ktg_engine_set_peers(self._h, rank, world, t0, t1, cb, None))
 
     def set_partition(self, rank: int, world: int, allreduce=None) -> None:
         cb = ALLREDUCE_CB(allreduce) if allreduce is not None else ALLREDUCE_CB()

@@ -1,0 +1,88 @@
+"""Fused reduce-scatter (ktg_engine_set_peers): each rank's support kernel
+sends every increment straight to the owner rank's buffer over peer memory;
+the exchange callback only all-gathers the owned spans. Two "virtual ranks"
+(two engines driven from two threads, one device) against the oracle,
+byte-exact -- the multi-GPU path's arithmetic and synchronisation protocol
+on the one GPU available to the tests."""
+import ctypes
+import threading
+
+import numpy as np
+import pytest
+
+import paper_2009_07929_b200 as kt
+from paper_2009_07929_b200 import truss
+
+pytestmark = pytest.mark.gpu
+
+
+def _run_ranks(g, world, ks):
+    engines = [kt.Engine(g) for _ in range(world)]
+    bufs = [e.support_buffers() for e in engines]
+    s0 = [b[0] for b in bufs]
+    s1 = [b[1] for b in bufs]
+    bar = threading.Barrier(world, timeout=120)
+    parts = [0] * world
+
+    def exchange_for(r):
+        def ex(phase, d_s, slots, span, d_tri, stream):
+            v = ctypes.c_uint64()
+            truss.device_copy(ctypes.addressof(v), ctypes.addressof(v), 0, stream)  # waits for the stream
+            bar.wait()
+            if phase == 0:  # every rank's previous prune is done
+                return
+            truss.device_copy(ctypes.addressof(v), d_tri, 8, stream)
+            parts[r] = v.value
+            bar.wait()
+            v.value = sum(parts)
+            truss.device_copy(d_tri, ctypes.addressof(v), 8, stream)
+            src = s0 if d_s == s0[r] else s1
+            for q in range(world):
+                lo = q * span
+                cnt = min(span, slots - lo)
+                if q != r and cnt > 0:
+                    truss.device_copy(d_s + 4 * lo, src[q] + 4 * lo, 4 * cnt, stream)
+            bar.wait()  # nobody prunes (zeroes) or adds again before all copies
+        return ex
+
+    for r, e in enumerate(engines):
+        e.set_peers(r, world, s0, s1, exchange_for(r))
+    out = [dict() for _ in range(world)]
+    errs = []
+
+    def body(r):
+        try:
+            for k in ks:
+                engines[r].reset()
+                hist = engines[r].run(k)
+                col, S = engines[r].read()
+                out[r][k] = (hist, col.copy(), S.copy(), engines[r].info()["triangles"])
+        except Exception as ex:  # pragma: no cover - reported below
+            errs.append(ex)
+            bar.abort()
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for e in engines:
+        e.close()
+    if errs:
+        raise errs[0]
+    return out
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_fused_reduce_scatter_virtual_ranks(port, world):
+    g = kt.rmat(13, 16, seed=4)
+    ks = (3, 5, 9)
+    out = _run_ranks(g, world, ks)
+    for k in ks:
+        col_e, S_e, hist_e = port.run_fixpoint(g, k, threads=8)
+        tri_e, _ = port.compute_supports(kt.ZeroTerminatedCsr(g.num_vertices, g.row_ptr, col_e), threads=8)
+        for r in range(world):
+            hist, col, S, tri = out[r][k]
+            assert hist == hist_e, (world, r, k)
+            assert np.array_equal(col, col_e) and np.array_equal(S, S_e), (world, r, k)
+            assert tri == tri_e, (world, r, k)
