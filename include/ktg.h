@@ -290,6 +290,12 @@ ktg_status ktg_engine_set_peers(ktg_engine* e, uint32_t rank, uint32_t world, ui
 /* cudaMemcpyAsync(cudaMemcpyDefault) + stream synchronize: a helper for
  * exchange callbacks written in a host language without CUDA bindings. */
 ktg_status ktg_device_copy(void* dst, const void* src, uint64_t bytes, void* stream);
+/* CUDA IPC of support buffers between rank processes (64-byte handles):
+ * ktg_ipc_handle on the owner, ktg_ipc_open on every peer (peer access is
+ * enabled lazily; NVLink peer memory on one node), ktg_ipc_close when done. */
+ktg_status ktg_ipc_handle(const void* d_ptr, uint8_t* out_64_bytes);
+ktg_status ktg_ipc_open(const uint8_t* handle_64_bytes, void** d_ptr);
+ktg_status ktg_ipc_close(void* d_ptr);
 
 #ifdef __cplusplus
 }

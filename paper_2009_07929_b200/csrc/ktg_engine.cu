@@ -1546,6 +1546,26 @@ ktg_status ktg_engine_set_peers(ktg_engine* e, uint32_t rank, uint32_t world, ui
   return KTG_OK;
 }
 
+ktg_status ktg_ipc_handle(const void* d_ptr, uint8_t* out_64_bytes) {
+  cudaIpcMemHandle_t h;
+  KTG_CUDA(cudaIpcGetMemHandle(&h, const_cast<void*>(d_ptr)));
+  static_assert(sizeof(h) == 64, "cudaIpcMemHandle_t is 64 bytes");
+  std::memcpy(out_64_bytes, &h, sizeof(h));
+  return KTG_OK;
+}
+
+ktg_status ktg_ipc_open(const uint8_t* handle_64_bytes, void** d_ptr) {
+  cudaIpcMemHandle_t h;
+  std::memcpy(&h, handle_64_bytes, sizeof(h));
+  KTG_CUDA(cudaIpcOpenMemHandle(d_ptr, h, cudaIpcMemLazyEnablePeerAccess));
+  return KTG_OK;
+}
+
+ktg_status ktg_ipc_close(void* d_ptr) {
+  KTG_CUDA(cudaIpcCloseMemHandle(d_ptr));
+  return KTG_OK;
+}
+
 ktg_status ktg_device_copy(void* dst, const void* src, uint64_t bytes, void* stream) {
   KTG_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDefault, (cudaStream_t)stream));
   KTG_CUDA(cudaStreamSynchronize((cudaStream_t)stream));

@@ -4,9 +4,13 @@ for rendezvous; the data path is the engine's own ncclAllReduce.
 Two ways the path shards:
   * K sweep   -- K values are independent fixpoints on a replicated graph:
                  split_k_values() hands each rank a share, no collective;
-  * one big fixpoint -- the support tasks are split t % world == rank; each
-                 round every rank all-reduces its partial supports (exact u32
-                 sums) and runs the same deterministic prune (engine_join()).
+  * one big fixpoint -- the support tasks are split into work-balanced
+                 ranges; each round every rank either all-reduces its partial
+                 supports (engine_join(): ncclAllReduce, exact u32 sums) or,
+                 fused (engine_join_fused()), sends every increment straight
+                 to the owner rank's buffer over NVLink peer memory during the
+                 support pass and only all-gathers the owned spans; then every
+                 rank runs the same deterministic prune.
 """
 from __future__ import annotations
 
@@ -15,7 +19,9 @@ from typing import List, Optional, Sequence
 import torch
 import torch.distributed as dist
 
-from .truss import Engine, nccl_unique_id
+import ctypes
+
+from .truss import Engine, device_copy, ipc_close, ipc_handle, ipc_open, nccl_unique_id
 
 
 def world_rank() -> tuple:
@@ -69,3 +75,42 @@ def sum_over_ranks(x: float, device: Optional[torch.device] = None) -> float:
     t = torch.tensor([float(x)], dtype=torch.float64, device=device)
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
+
+
+def engine_join_fused(engine: Engine, group: Optional[dist.ProcessGroup] = None) -> list:
+    """Fused reduce-scatter (ktg_engine_set_peers): exchanges the support
+    buffers' CUDA IPC handles (collective), maps every peer's buffers, and
+    installs the per-round exchange (barrier; all-gather of the owned spans
+    by peer copies; sum of the round's triangle count). Call after
+    engine.load(). Returns the mapped peer pointers (ipc_close them after the
+    engine is done)."""
+    world, rank = world_rank()
+    s0, s1, _ = engine.support_buffers()
+    mine = (ipc_handle(s0), ipc_handle(s1))
+    allh = [None] * world
+    dist.all_gather_object(allh, mine, group=group)
+    p0 = [s0 if q == rank else ipc_open(allh[q][0]) for q in range(world)]
+    p1 = [s1 if q == rank else ipc_open(allh[q][1]) for q in range(world)]
+    dev = "cuda" if dist.get_backend(group) == "nccl" else "cpu"
+
+    def exchange(phase, d_s, slots, span, d_tri, stream):
+        v = ctypes.c_uint64()
+        device_copy(ctypes.addressof(v), ctypes.addressof(v), 0, stream)  # wait for this rank's stream
+        dist.barrier(group=group)
+        if phase == 0:  # every rank's previous prune (buffer zeroing) is done
+            return
+        device_copy(ctypes.addressof(v), d_tri, 8, stream)
+        t = torch.tensor([v.value], dtype=torch.int64, device=dev)
+        dist.all_reduce(t, group=group)
+        v.value = int(t.item())
+        device_copy(d_tri, ctypes.addressof(v), 8, stream)
+        src = p0 if d_s == s0 else p1
+        for q in range(world):
+            lo = q * span
+            cnt = min(span, slots - lo)
+            if q != rank and cnt > 0:
+                device_copy(d_s + 4 * lo, src[q] + 4 * lo, 4 * cnt, stream)
+        dist.barrier(group=group)  # no rank zeroes or adds again before all copies
+
+    engine.set_peers(rank, world, p0, p1, exchange)
+    return [p for q, p in enumerate(p0 + p1) if q % world != rank]

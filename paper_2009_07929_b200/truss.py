@@ -212,6 +212,9 @@ def lib():
         L.ktg_engine_support_buffers.argtypes = [_vp, P(_vp), P(_vp), P(_u64)]
         L.ktg_engine_set_peers.argtypes = [_vp, _u32, _u32, _vp, _vp, PEER_CB, _vp]
         L.ktg_device_copy.argtypes = [_vp, _vp, _u64, _vp]
+        L.ktg_ipc_handle.argtypes = [_vp, _vp]
+        L.ktg_ipc_open.argtypes = [_vp, P(_vp)]
+        L.ktg_ipc_close.argtypes = [_vp]
         L.ktg_nccl_unique_id.argtypes = [_vp]
         L.ktg_engine_set_nccl.argtypes = [_vp, _u32, _u32, _vp]
         _configured = True
@@ -489,6 +492,25 @@ def device_copy(dst: int, src: int, nbytes: int, stream: Optional[int] = None) -
     """cudaMemcpyAsync(cudaMemcpyDefault) + synchronize (device or host
     pointers), for peer-exchange callbacks."""
     _check(lib().ktg_device_copy(dst, src, nbytes, stream))
+
+
+def ipc_handle(d_ptr: int) -> bytes:
+    """64-byte CUDA IPC handle of a device allocation (a support buffer)."""
+    buf = (ctypes.c_uint8 * 64)()
+    _check(lib().ktg_ipc_handle(d_ptr, buf))
+    return bytes(buf)
+
+
+def ipc_open(handle: bytes) -> int:
+    """Maps a peer process's allocation into this one; returns the pointer."""
+    buf = (ctypes.c_uint8 * 64).from_buffer_copy(handle)
+    p = _vp()
+    _check(lib().ktg_ipc_open(buf, ctypes.byref(p)))
+    return p.value
+
+
+def ipc_close(d_ptr: int) -> None:
+    _check(lib().ktg_ipc_close(d_ptr))
 
 
 def nccl_unique_id() -> bytes:

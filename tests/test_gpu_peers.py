@@ -86,3 +86,64 @@ def test_fused_reduce_scatter_virtual_ranks(port, world):
             assert hist == hist_e, (world, r, k)
             assert np.array_equal(col, col_e) and np.array_equal(S, S_e), (world, r, k)
             assert tri == tri_e, (world, r, k)
+
+
+def _proc(rank, world, port, ks, q):
+    import os
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    import torch.distributed as dist
+
+    import paper_2009_07929_b200 as kt2
+    from paper_2009_07929_b200 import dist as kd
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        g = kt2.rmat(13, 16, seed=4)
+        e = kt2.Engine(g)
+        mapped = kd.engine_join_fused(e)
+        res = {}
+        for k in ks:
+            e.reset()
+            hist = e.run(k)
+            col, S = e.read()
+            res[k] = (hist, col.copy(), S.copy())
+        dist.barrier()
+        e.close()
+        for p in mapped:
+            kt2.truss.ipc_close(p)
+        q.put((rank, res))
+    except Exception as ex:  # surfaced by the parent
+        q.put((rank, repr(ex)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_fused_reduce_scatter_two_processes_ipc(port):
+    """The multi-process wiring (dist.engine_join_fused): CUDA IPC handles of
+    the support buffers exchanged over torch.distributed, peer atomics into
+    the other process's buffers, gloo barriers -- two rank processes sharing
+    the one device, byte-exact against the oracle."""
+    import socket
+
+    import torch.multiprocessing as mp
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    p = s.getsockname()[1]
+    s.close()
+    ks = (3, 6)
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_proc, args=(r, 2, p, ks, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    out = dict(q.get(timeout=300) for _ in procs)
+    for pr in procs:
+        pr.join(timeout=60)
+    g = kt.rmat(13, 16, seed=4)
+    for r in range(2):
+        assert not isinstance(out[r], str), out[r]
+        for k in ks:
+            col_e, S_e, hist_e = port.run_fixpoint(g, k, threads=8)
+            hist, col, S = out[r][k]
+            assert hist == hist_e and np.array_equal(col, col_e) and np.array_equal(S, S_e), (r, k)
