@@ -72,6 +72,9 @@ def parse():
                     help="sweep: K sweep 3..K_max (K split across ranks); fixpoint: one fixpoint per step "
                          "at --k (0 = K_max), edge-partitioned over NCCL across ranks")
     ap.add_argument("--k", type=int, default=0)
+    ap.add_argument("--exchange", default="nccl", choices=["nccl", "fused"],
+                    help="fixpoint mode, N>1: ncclAllReduce of partial supports, or the reduce-scatter fused "
+                         "into the support kernel (peer atomics + span all-gather over CUDA IPC)")
     ap.add_argument("--graph", default="rmat", choices=["rmat", "er"],
                     help="er: Erdős–Rényi with 2^scale vertices and ef*2^scale draws (SURVEY §8(d))")
     return ap.parse_args()
@@ -512,7 +515,10 @@ def run_fixpoint_mode(args):
     eng = kt.Engine(g, stream=stream.cuda_stream)
     k = args.k or KNOWN_KMAX.get(kmax_key(args)) or eng.kmax()
     if world > 1:
-        kd.engine_join(eng)
+        if args.exchange == "fused":
+            kd.engine_join_fused(eng)
+        else:
+            kd.engine_join(eng)
     eng.reset()
     hist = eng.run(k)
     # carried-support rounds on one rank (13 launches per round + 2 + 4);
@@ -593,7 +599,10 @@ def run_fixpoint_mode(args):
                        "n": n, "m": m, "slots": slots, "k": k, "rounds": len(hist),
                        "l2": "512 MiB memset between timed steps; inputs > L2" if slots * 4 > 126e6 else
                              "512 MiB memset between timed steps",
-                       "parallelism": f"edge-partitioned x{world} (ncclAllReduce of S per round)" if world > 1
+                       "parallelism": (f"edge-partitioned x{world} (" + ("support kernel fused with the reduce-scatter, span "
+                                                                     "all-gather" if args.exchange == "fused" else
+                                                                     "ncclAllReduce of S") + " per round)")
+                       if world > 1
                                       else "single"},
             "time_to_fixpoint_ms": ms, "me_per_s": value / 1e6,
             "e2e": {"value": m / (e2e_ms / 1e3), "unit": "edges/s", "h2d_bytes_per_step": (n + 2 + slots) * 4,
