@@ -356,6 +356,8 @@ def main():
     pin_col[:] = g.col_idx
     hg = kt.ZeroTerminatedCsr(n, pin_rp, pin_col)
     e2e_ms, d2h = [], 0
+    if mine:  # untimed warm-up call: the cached host-API engine and the pinned result pool
+        kt.ktruss(hg, mine[0])
     barrier()
     for _ in range(max(1, args.e2e_steps)):
         torch.cuda.synchronize()
@@ -555,6 +557,10 @@ def run_fixpoint_mode(args):
     keep[0].numpy().view(np.uint32)[:] = g.row_ptr
     keep[1].numpy().view(np.uint32)[:] = g.col_idx
     hg = kt.ZeroTerminatedCsr(n, keep[0].numpy().view(np.uint32), keep[1].numpy().view(np.uint32))
+    eng.load(hg)  # untimed warm-up of the same sequence (pinned result pool)
+    eng.run(k)
+    edges = eng.extract()
+    del edges
     torch.cuda.synchronize()
     t = time.perf_counter()
     eng.load(hg)
