@@ -300,9 +300,17 @@ class _ResultPool:
     COPY_OUT_BYTES = 4 << 20
 
     def __init__(self):
+        import threading
         self._owners = []
+        # the C engines are per thread, so calls may run concurrently: the
+        # free check and the caller's reference must not interleave
+        self._lock = threading.Lock()
 
     def take(self, cap: int):
+        with self._lock:
+            return self._take(cap)
+
+    def _take(self, cap: int):
         words = 3 * max(cap, 1)
         for owner in self._owners:
             # refs: the pool list, this loop variable, getrefcount's argument
