@@ -5,6 +5,8 @@ sys.path.insert(0, ".")
 import paper_2009_07929_b200 as kt
 g = kt.rmat(int(os.environ.get("SCALE", "20")))
 ks = [3, 5, 10, 20, 30, 45, 60, 80, 100, 110, 120, 135, 150, 165, 180, 200, 215, 230, 260, 304]
+if os.environ.get("KS"):
+    ks = [int(x) for x in os.environ["KS"].split(",")]
 # RATIO_VAR=KTG_DELTA_RATIO0 scans round 0 from pristine only
 var = os.environ.get("RATIO_VAR", "KTG_DELTA_RATIO")
 ratios = sys.argv[1:] or ["0", "0.05", "0.1", "0.2", "0.5", "1", "1e9"]
