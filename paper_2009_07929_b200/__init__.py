@@ -6,13 +6,14 @@ compute path is the sm_100a library libktg.so behind the C ABI in
 include/ktg.h -- there is no CPU fallback.
 """
 from . import errors, graph
-from .graph import ZeroTerminatedCsr, csr_from_pairs, erdos_renyi, extract_edges, rmat, validate_csr
+from .graph import (ZeroTerminatedCsr, csr_from_pairs, erdos_renyi, extract_edges, rmat, rmat_cliques,
+                    validate_csr)
 from .truss import (Engine, KmaxResult, Strategy, SupportArray, SupportWidth, TrussOptions, TrussResult,
                     compute_supports, detail, hardware_threads, intersect_tails, kmax_search, ktruss,
                     prune_edges, reset_supports, run_fixpoint, strategy_from_string, to_string)
 
 __all__ = [
-    "errors", "graph", "ZeroTerminatedCsr", "csr_from_pairs", "erdos_renyi", "extract_edges", "rmat",
+    "errors", "graph", "ZeroTerminatedCsr", "csr_from_pairs", "erdos_renyi", "extract_edges", "rmat", "rmat_cliques",
     "validate_csr", "Engine", "KmaxResult", "Strategy", "SupportArray", "SupportWidth", "TrussOptions",
     "TrussResult", "compute_supports", "detail", "hardware_threads", "intersect_tails", "kmax_search",
     "ktruss", "prune_edges", "reset_supports", "run_fixpoint", "strategy_from_string", "to_string",

@@ -373,6 +373,7 @@ ktg_status read_state(ktg_engine* e) {
 }
 
 __global__ void k_set_live(DevState* st, unsigned long long live) { st->live = live; }
+__global__ void k_set_rqcap(DevState* st, unsigned long long cap) { st->rq_cap = cap; }
 __global__ void k_clear_heavy(DevState* st) { st->nheavy = 0; }
 
 // Per-layout structures once L.row_ptr / L.col hold a CSR: live degrees,
@@ -615,8 +616,14 @@ ktg_status build_sym(ktg_engine* e) {
   unsigned long long cap = 0;
   KTG_CUDA(cudaMemcpyAsync(&cap, e->d_workL, 8, cudaMemcpyDeviceToHost, s));
   KTG_CUDA(cudaStreamSynchronize(s));
+  // the exact worst case (every edge's pieces at pristine degrees) can be
+  // tens of GB on dense graphs; cap the queue at one piece per edge -- a
+  // round whose removals could need more recomputes instead (k_decide)
+  cap = std::min<unsigned long long>(cap, std::max<unsigned long long>(1ull << 20, m));
   e->rq_cap = cap;
   KTG_TRY(e->rq.ensure(cap));
+  k_set_rqcap<<<1, 1, 0, s>>>(e->d_st, cap);
+  KTG_CUDA(cudaGetLastError());
   e->sym_ready = true;
   e->pristine = true;
   return build_a22(e);

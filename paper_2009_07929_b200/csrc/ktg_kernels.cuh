@@ -69,6 +69,7 @@ struct DevState {
   unsigned long long last_kcost;
   double delta_ratio0;               // the same for round 0 of a run from the pristine graph
   unsigned int dq_lo, dq_hi;         // this rank's diagonal support tasks: chunks [dq_lo, dq_hi)
+  unsigned long long rq_cap;         // delta piece queue capacity (a round that could exceed it recomputes)
 };
 
 struct Graph {
@@ -1537,8 +1538,10 @@ __global__ void k_set_pristine(DevState* st) { st->pristine = 1; }
 // One thread: this round's removal count is final; choose carry vs recompute.
 __global__ void k_decide(DevState* st) {
   if (st->mode == 1) st->keep_cost = st->live_cost > st->delta_cost ? st->live_cost - st->delta_cost : 0;
+  // pieces queued <= delta_cost / kDeltaPiece + removed: carry only if they fit
   st->carry = (st->inc && st->removed != 0 &&
-               (double)st->delta_cost <= (st->pristine ? st->delta_ratio0 : st->delta_ratio) * (double)st->keep_cost)
+               (double)st->delta_cost <= (st->pristine ? st->delta_ratio0 : st->delta_ratio) * (double)st->keep_cost &&
+               st->delta_cost / kDeltaPiece + st->removed <= st->rq_cap)
                   ? 1u
                   : 0u;
 }

@@ -172,6 +172,46 @@ def rmat(scale: int, edgefactor: int = 16, seed: int = 42,
     return _raw_to_csr(h)
 
 
+def clique_members(n_labels: int, c: int, seed: int) -> np.ndarray:
+    """c distinct labels in [0, n_labels): the first c positions of a
+    partial Fisher-Yates shuffle driven by numpy's MT19937(seed)."""
+    if c > n_labels:
+        raise errors.InvalidParameterError("clique larger than the vertex set")
+    rng = np.random.Generator(np.random.MT19937(seed))
+    draws = rng.integers(0, np.arange(n_labels, n_labels - c, -1, dtype=np.int64), dtype=np.int64)
+    chosen = {}
+    out = np.empty(c, np.int64)
+    for i in range(c):  # swap position i with i + draws[i] (sparse permutation)
+        j = i + int(draws[i])
+        out[i] = chosen.get(j, j)
+        chosen[j] = chosen.get(i, i)
+    return out.astype(np.uint64)
+
+
+def rmat_cliques(scale: int, edgefactor: int = 32, seed: int = 42, sizes=(128, 256, 512, 1024),
+                 a: float = 0.57, b: float = 0.19, c: float = 0.19) -> ZeroTerminatedCsr:
+    """BASELINE.json configs[4] (SURVEY.md §8(d) "planted cliques"): the
+    R-MAT raw pairs plus, before canonicalize, every pair of each planted
+    clique; clique of size c_i uses clique_members(2^scale, c_i, seed + i).
+    K_max >= max(sizes), with many prune rounds."""
+    lib = _g()
+    h = ctypes.c_void_p()
+    rc = lib.ktgg_rmat_raw(scale, edgefactor, seed, a, b, c, ctypes.byref(h))
+    if rc:
+        _raise(rc)
+    try:
+        m = int(lib.ktgg_raw_count(h))
+        raw = np.ctypeslib.as_array(lib.ktgg_raw_pairs(h), shape=(2 * m,)).reshape(m, 2).astype(np.uint64)
+    finally:
+        lib.ktgg_raw_free(h)
+    parts = [raw]
+    for i, cs in enumerate(sizes):
+        mem = clique_members(1 << scale, int(cs), seed + i)
+        iu, ju = np.triu_indices(len(mem), 1)
+        parts.append(np.stack([mem[iu], mem[ju]], axis=1))
+    return csr_from_pairs(np.concatenate(parts))
+
+
 def erdos_renyi(log_n: int, m: int, seed: int = 42) -> ZeroTerminatedCsr:
     """Erdős–Rényi per SURVEY.md §8(d): m uniform endpoint draws, canonicalized."""
     lib = _g()

@@ -204,3 +204,19 @@ def test_incremental_sweep_equals_pristine(s14, port):
     for rec in recs[::7] + [recs[-2]]:
         e, _ = port.truss_edges(s14, rec["k"], threads=8)
         assert np.array_equal(rec["truss"].edges, e), rec["k"]
+
+
+def test_planted_cliques_deep_kmax(port):
+    """configs[4] semantics at a small scale (deep K_max, many prune rounds):
+    byte-exact fixpoints and K_max."""
+    g = kt.rmat_cliques(12, 16, 42, sizes=(24, 64))
+    km = kt.kmax_search(g)
+    assert km.k_max == port.kmax(g, threads=8) == 64
+    eng = kt.Engine(g)
+    for k in (3, 30, 64, 65):
+        eng.reset()
+        hist = eng.run(k)
+        col, S = eng.read()
+        col_e, S_e, hist_e = port.run_fixpoint(g, k, threads=8)
+        assert hist == hist_e and np.array_equal(col, col_e) and np.array_equal(S, S_e), k
+    eng.close()

@@ -130,3 +130,16 @@ def test_port_matches_reference_on_corpus(port, ref):
             c_r, s_r, h_r, _ = ref.run_fixpoint(g, k)
             c_p, s_p, h_p = port.run_fixpoint(g, k)
             assert h_r == h_p and np.array_equal(c_r, c_p) and np.array_equal(s_r, s_p), (i, k)
+
+
+def test_planted_cliques_config(port):
+    """BASELINE configs[4] generator (graph.rmat_cliques): deterministic,
+    every clique pair present, K_max = the largest planted clique when it
+    dominates the R-MAT part."""
+    from paper_2009_07929_b200.graph import clique_members
+    g1 = graph.rmat_cliques(10, 8, 42, sizes=(16, 40))
+    g2 = graph.rmat_cliques(10, 8, 42, sizes=(16, 40))
+    assert np.array_equal(g1.col_idx, g2.col_idx) and np.array_equal(g1.row_ptr, g2.row_ptr)
+    m = clique_members(1 << 10, 40, 43)
+    assert len(set(m.tolist())) == 40
+    assert port.kmax(g1, threads=4) == 40
