@@ -41,18 +41,23 @@ METRIC = "K-truss time-to-fixpoint (ms) & edges/sec at 1/2/4/8 B200; achieved HB
 # K_max of the pinned configs (reference-measured; also
 # asserted by tests/test_gpu_large.py) -- lets the reference arm skip its
 # ~200 s CPU kmax_search.
-KNOWN_KMAX = {(14, 16, 42): 79, (20, 16, 42): 304, (24, 16, 42): 935, ("er", 22, 16, 42): 3}
+KNOWN_KMAX = {(14, 16, 42): 79, (20, 16, 42): 304, (24, 16, 42): 935, ("er", 22, 16, 42): 3,
+              ("cliques", 22, 32, 42): 1057, ("cliques", 24, 32, 42): 1654}
 
 
 def make_graph(args):
     import paper_2009_07929_b200 as kt
     if args.graph == "er":
         return kt.erdos_renyi(args.scale, args.ef << args.scale, args.seed)
+    if args.graph == "cliques":
+        return kt.rmat_cliques(args.scale, args.ef, args.seed)
     return kt.rmat(args.scale, args.ef, args.seed)
 
 
 def kmax_key(args):
-    return ("er", args.scale, args.ef, args.seed) if args.graph == "er" else (args.scale, args.ef, args.seed)
+    if args.graph != "rmat":
+        return (args.graph, args.scale, args.ef, args.seed)
+    return (args.scale, args.ef, args.seed)
 
 
 def parse():
@@ -75,8 +80,9 @@ def parse():
     ap.add_argument("--exchange", default="nccl", choices=["nccl", "fused"],
                     help="fixpoint mode, N>1: ncclAllReduce of partial supports, or the reduce-scatter fused "
                          "into the support kernel (peer atomics + span all-gather over CUDA IPC)")
-    ap.add_argument("--graph", default="rmat", choices=["rmat", "er"],
-                    help="er: Erdős–Rényi with 2^scale vertices and ef*2^scale draws (SURVEY §8(d))")
+    ap.add_argument("--graph", default="rmat", choices=["rmat", "er", "cliques"],
+                    help="er: Erdős–Rényi with 2^scale vertices and ef*2^scale draws (SURVEY §8(d)); "
+                         "cliques: R-MAT plus planted cliques of 128..1024 (configs[4])")
     return ap.parse_args()
 
 
@@ -601,6 +607,8 @@ def run_fixpoint_mode(args):
             "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "u32", "data": "synthetic",
             "config": {"workload": (f"er-2^{args.scale}-{args.ef}x K={k} fixpoint" if args.graph == "er" else
+                                    f"rmat-s{args.scale}-ef{args.ef}+cliques(128..1024) K={k} fixpoint"
+                                    if args.graph == "cliques" else
                                     f"rmat-s{args.scale}-ef{args.ef} K={k} fixpoint"),
                        "n": n, "m": m, "slots": slots, "k": k, "rounds": len(hist),
                        "l2": "512 MiB memset between timed steps; inputs > L2" if slots * 4 > 126e6 else
