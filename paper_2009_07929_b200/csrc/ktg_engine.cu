@@ -1217,7 +1217,15 @@ struct TmpEngine {
   }
 };
 
-thread_local ktg_engine* t_cached[64] = {};
+// One cached engine per (thread, device) for the host-buffer entry points;
+// destroyed when the thread exits (a thread pool sweeping K values keeps its
+// engines warm, and no engine outlives its thread).
+struct ThreadEngines {
+  ktg_engine* e[64] = {};
+  ktg_engine*& operator[](int i) { return e[i]; }
+  ~ThreadEngines();
+};
+thread_local ThreadEngines t_cached;
 
 ktg_status tmp_engine(const ktg_options* opt, const uint32_t* row_ptr, uint32_t n, const uint32_t* col,
                       uint64_t slots, bool pristine, bool allow_reorient, TmpEngine& t) {
@@ -1747,3 +1755,13 @@ ktg_status ktg_kmax_search(const uint32_t* row_ptr, uint32_t n, const uint32_t* 
 }
 
 }  // extern "C"
+
+namespace {
+ThreadEngines::~ThreadEngines() {
+  for (ktg_engine*& x : e)
+    if (x) {
+      ktg_engine_destroy(x);
+      x = nullptr;
+    }
+}
+}  // namespace

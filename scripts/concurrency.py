@@ -6,7 +6,8 @@ import numpy as np, torch
 import paper_2009_07929_b200 as kt
 g = kt.rmat(20)
 ks = list(range(3, 305))
-for P in (1, 2, 3, 4):
+PS = [int(x) for x in sys.argv[1].split(",")] if len(sys.argv) > 1 else [1, 2, 3, 4]
+for P in PS:
     streams = [torch.cuda.Stream() for _ in range(P)]
     engs = [kt.Engine(g, stream=s.cuda_stream) for s in streams]
     def sweep():
@@ -21,7 +22,7 @@ n, slots = g.num_vertices, g.total_slots()
 keep = (torch.empty(n + 2, dtype=torch.int32, pin_memory=True), torch.empty(slots, dtype=torch.int32, pin_memory=True))
 keep[0].numpy().view(np.uint32)[:] = g.row_ptr; keep[1].numpy().view(np.uint32)[:] = g.col_idx
 hg = kt.ZeroTerminatedCsr(n, keep[0].numpy().view(np.uint32), keep[1].numpy().view(np.uint32))
-for T in (1, 2, 4):
+for T in ((1, 2, 4) if len(sys.argv) <= 2 else [int(x) for x in sys.argv[2].split(",") if x]):
     def work(part):
         for k in part:
             r = kt.ktruss(hg, k)
