@@ -143,6 +143,18 @@ class ClockSampler:
                 "samples": len(self.samples)}
 
 
+def cpu_model() -> str:
+    """The host CPU's model name (the reference timing's hardware)."""
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
 def k_values(kmax: int, stride: int):
     ks = list(range(3, kmax + 1, stride))
     if ks[-1] != kmax:
@@ -233,7 +245,7 @@ def run_reference(args):
         "config": {"workload": f"rmat-s{args.scale}-ef{args.ef} K-sweep 3..{ks[-1]} (pristine per K)",
                    "n": g.num_vertices, "m": g.num_edges, "k_values": len(ks), "parallelism": "cpu-omp"},
         "cpu_baseline": {"value": value, "unit": "edges/s", "cores": threads, "kind": "reference",
-                         "sample": sample},
+                         "sample": sample, "cpu": cpu_model()},
         "e2e": {"value": value, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -472,7 +484,8 @@ def main():
             v, done = cpu_sample(g, ks, args.cpu_budget_s, threads)
             cpu = {"value": v, "unit": "edges/s", "cores": threads, "kind": "reference",
                    "sample": "reference run_fixpoint (Strategy::Fine) from pristine at K in "
-                             f"{[k for k, _ in done]} ({', '.join(f'{ms:.0f}' for _, ms in done)} ms)"}
+                             f"{[k for k, _ in done]} ({', '.join(f'{ms:.0f}' for _, ms in done)} ms)",
+                   "cpu": cpu_model()}
         except Exception as ex:  # reference library not built
             cpu = {"value": None, "unit": "edges/s", "cores": 0, "kind": "reference",
                    "sample": f"unavailable: {ex}"}
