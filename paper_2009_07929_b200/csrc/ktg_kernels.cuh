@@ -1584,11 +1584,30 @@ __device__ __forceinline__ void delta_edge(const Graph& g, const Sym& y, uint32_
   const uint32_t* __restrict__ A = y.nbr + oa;
   const uint32_t* __restrict__ B = y.nbr + ob;
   hi = min(hi, la);
+  if (lo >= hi) return;
   const uint32_t bmin = B[0], bmax = B[lb - 1];
-  for (uint32_t i = lo + lane; i < hi; i += 32) {
-    const uint32_t w = A[i];
-    if (w < bmin || w > bmax) continue;
-    const uint32_t j = lb_run(B, lb, w);
+  // long B: lane l holds the last element of bucket l of 32 equal buckets,
+  // so an element's bucket comes from 5 shuffles and its global binary
+  // search covers lb/32 entries (5 fewer dependent loads per element)
+  const bool coarse = lb >= 256;
+  const uint32_t samp = coarse ? B[(uint32_t)(((uint64_t)(lane + 1) * lb) >> 5) - 1] : 0u;
+  for (uint32_t b0 = lo; b0 < hi; b0 += 32) {  // warp-uniform trip count (shuffles)
+    const uint32_t i = b0 + lane;
+    const bool act = i < hi;
+    const uint32_t w = act ? A[i] : 0u;
+    uint32_t jlo = 0, jn = lb;
+    if (coarse) {
+      uint32_t k = 0;  // first bucket whose last element >= w (w <= bmax = last of bucket 31)
+#pragma unroll
+      for (uint32_t step = 16; step; step >>= 1) {
+        const uint32_t sv = __shfl_sync(0xffffffffu, samp, k + step - 1);
+        if (sv < w) k += step;
+      }
+      jlo = (uint32_t)(((uint64_t)k * lb) >> 5);
+      jn = (uint32_t)(((uint64_t)(k + 1) * lb) >> 5) - jlo;
+    }
+    if (!act || w < bmin || w > bmax) continue;
+    const uint32_t j = jlo + lb_run(B + jlo, jn, w);
     if (j < lb && B[j] == w) {
       const uint32_t ea = y.eid[oa + i], eb = y.eid[ob + j];
       const bool da = y.dead[ea], db = y.dead[eb];
