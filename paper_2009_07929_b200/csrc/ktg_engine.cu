@@ -877,7 +877,7 @@ ktg_status enqueue_round(ktg_engine* e, bool graph_mode, cudaGraphConditionalHan
     k_inc_rows<0><<<e->prune_grid, kPruneThreads, 0, s>>>(g, y);
     k_inc_rows<1><<<e->heavy_grid, kPruneThreads, 0, s>>>(g, y);
     k_inc_sym<0><<<e->prune_grid, kPruneThreads, 0, s>>>(g, y);
-    k_inc_sym<1><<<e->heavy_grid, kPruneThreads, 0, s>>>(g, y);
+    k_inc_sym<1><<<e->heavy_grid, kSymHeavyThreads, 0, s>>>(g, y);
     k_inc_zero<<<4 * e->num_sms, 256, 0, s>>>(g);
     k_control_inc<<<1, 1, 0, s>>>(e->d_st, e->d_hist, handle, graph_mode ? 1 : 0);
     KTG_CUDA(cudaGetLastError());

@@ -1771,11 +1771,15 @@ k_inc_rows(Graph g, Sym y) {
 }
 
 // Symmetric rows that lost an edge drop their dead entries (stable).
+// Heavy rows are few (the hubs), so their kernel runs kSymHeavyThreads-wide
+// CTAs: a row takes 4x fewer dependent tile steps than with 256 threads.
+constexpr int kSymHeavyThreads = 1024;
 template <int HEAVY>
-__global__ void __launch_bounds__(kPruneThreads)
+__global__ void __launch_bounds__(HEAVY ? kSymHeavyThreads : kPruneThreads)
 k_inc_sym(Graph g, Sym y) {
   constexpr int EPT = HEAVY ? 4 : 1;
-  constexpr int NW = kPruneThreads / 32;
+  constexpr int BT = HEAVY ? kSymHeavyThreads : kPruneThreads;
+  constexpr int NW = BT / 32;
   __shared__ uint32_t red[NW];
   __shared__ uint32_t tot_s;
   if (g.st->removed == 0) return;
@@ -1793,7 +1797,7 @@ k_inc_sym(Graph g, Sym y) {
     }
     const unsigned long long base = y.ptr[v];
     uint32_t write = 0;
-    constexpr uint32_t TILE = HEAVY ? EPT * kPruneThreads : 32;
+    constexpr uint32_t TILE = HEAVY ? EPT * BT : 32;
     for (uint32_t off = 0; off < d; off += TILE) {
       uint32_t w[EPT], ev[EPT];
       bool keep[EPT];
