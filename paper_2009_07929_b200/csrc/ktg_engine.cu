@@ -792,7 +792,7 @@ ktg_status publish(ktg_engine* e) {
     k_clear_heavy<<<1, 1, 0, s>>>(e->d_st);
     k_publish_inc<0><<<e->prune_grid, kPruneThreads, 0, s>>>(g, C.col_p.p, C.deg_p.p, e->dead.p, e->pos_of.p,
                                                             e->wl.S0.p);
-    k_publish_inc<1><<<e->heavy_grid, kPruneThreads, 0, s>>>(g, C.col_p.p, C.deg_p.p, e->dead.p, e->pos_of.p,
+    k_publish_inc<1><<<e->heavy_grid, kSymHeavyThreads, 0, s>>>(g, C.col_p.p, C.deg_p.p, e->dead.p, e->pos_of.p,
                                                             e->wl.S0.p);
     k_clear_heavy<<<1, 1, 0, s>>>(e->d_st);
     KTG_CUDA(cudaGetLastError());

@@ -1860,12 +1860,13 @@ k_inc_sym(Graph g, Sym y) {
 // take their support from the working slot pos_of[s]. Warp per row up to
 // kHeavyRow (HEAVY = 0, longer rows queued), CTA per longer row (HEAVY = 1).
 template <int HEAVY>
-__global__ void __launch_bounds__(kPruneThreads)
+__global__ void __launch_bounds__(HEAVY ? kSymHeavyThreads : kPruneThreads)
 k_publish_inc(Graph c, const uint32_t* __restrict__ col_p, const uint32_t* __restrict__ deg_p,
               const uint8_t* __restrict__ dead, const uint32_t* __restrict__ pos_of,
               const uint32_t* __restrict__ Sw) {
   constexpr int EPT = HEAVY ? 4 : 1;
-  constexpr int NW = kPruneThreads / 32;
+  constexpr int BT = HEAVY ? kSymHeavyThreads : kPruneThreads;
+  constexpr int NW = BT / 32;
   __shared__ uint32_t red[NW];
   __shared__ uint32_t tot_s;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -1882,7 +1883,7 @@ k_publish_inc(Graph c, const uint32_t* __restrict__ col_p, const uint32_t* __res
     }
     const uint32_t base = c.row_ptr[r];
     uint32_t write = 0;
-    constexpr uint32_t TILE = HEAVY ? EPT * kPruneThreads : 32;
+    constexpr uint32_t TILE = HEAVY ? EPT * BT : 32;
     for (uint32_t off = 0; off < d; off += TILE) {
       uint32_t cv[EPT], sv[EPT];
       bool keep[EPT];
