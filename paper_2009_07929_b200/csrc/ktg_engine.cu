@@ -806,7 +806,7 @@ ktg_status publish(ktg_engine* e) {
   k_clear_heavy<<<1, 1, 0, s>>>(e->d_st);
   Graph g = e->graph_of(C);
   k_prune_light<1><<<e->prune_grid, kPruneThreads, 0, s>>>(g, 0);
-  k_prune_heavy<1><<<e->heavy_grid, kPruneThreads, 0, s>>>(g, 0);
+  k_prune_heavy<1><<<e->heavy_grid, kSymHeavyThreads, 0, s>>>(g, 0);
   k_clear_heavy<<<1, 1, 0, s>>>(e->d_st);
   KTG_CUDA(cudaGetLastError());
   e->caller_stale = false;
@@ -875,7 +875,7 @@ ktg_status enqueue_round(ktg_engine* e, bool graph_mode, cudaGraphConditionalHan
     k_delta<<<e->prune_grid, kPruneThreads, 0, s>>>(g, y);
     k_delta_big<<<e->prune_grid, kPruneThreads, 0, s>>>(g, y);
     k_inc_rows<0><<<e->prune_grid, kPruneThreads, 0, s>>>(g, y);
-    k_inc_rows<1><<<e->heavy_grid, kPruneThreads, 0, s>>>(g, y);
+    k_inc_rows<1><<<e->heavy_grid, kSymHeavyThreads, 0, s>>>(g, y);
     k_inc_sym<0><<<e->prune_grid, kPruneThreads, 0, s>>>(g, y);
     k_inc_sym<1><<<e->heavy_grid, kSymHeavyThreads, 0, s>>>(g, y);
     k_inc_zero<<<4 * e->num_sms, 256, 0, s>>>(g);
@@ -906,7 +906,7 @@ ktg_status enqueue_round(ktg_engine* e, bool graph_mode, cudaGraphConditionalHan
     }
   }
   k_prune_light<0><<<e->prune_grid, kPruneThreads, 0, s>>>(g, fused);
-  k_prune_heavy<0><<<e->heavy_grid, kPruneThreads, 0, s>>>(g, fused);
+  k_prune_heavy<0><<<e->heavy_grid, kSymHeavyThreads, 0, s>>>(g, fused);
   k_control<<<1, 1, 0, s>>>(e->d_st, e->d_hist, handle, graph_mode ? 1 : 0);
   KTG_CUDA(cudaGetLastError());
   return KTG_OK;
@@ -1668,7 +1668,7 @@ ktg_status ktg_prune_edges(const uint32_t* row_ptr, uint32_t n, uint32_t* col_id
   KTG_TRY(begin_run(e, k, 0));
   Graph g = e->graph_of(C);
   k_prune_light<0><<<e->prune_grid, kPruneThreads, 0, e->stream>>>(g, 0);
-  k_prune_heavy<0><<<e->heavy_grid, kPruneThreads, 0, e->stream>>>(g, 0);
+  k_prune_heavy<0><<<e->heavy_grid, kSymHeavyThreads, 0, e->stream>>>(g, 0);
   KTG_CUDA(cudaGetLastError());
   KTG_TRY(read_state(e));
   KTG_CUDA(cudaMemcpy(col_idx, C.col.p, slots * 4, cudaMemcpyDeviceToHost));

@@ -23,6 +23,9 @@ constexpr int kChunk = 512;          // slots per staged chunk (P)
 constexpr int kSupportThreads = 256; // threads per support CTA
 constexpr int kPruneThreads = 256;
 constexpr int kHeavyRow = 2048;      // rows longer than this are pruned by a CTA
+// Heavy rows are few (the hubs), so their CTA-per-row kernels run 1024-wide:
+// a row takes 4x fewer dependent tile steps than with 256 threads.
+constexpr int kSymHeavyThreads = 1024;
 constexpr uint32_t kClipMin = 16;    // clip N+(j) by binary search above this degree
 constexpr uint32_t kScanRatio = 4;   // scan N+(j) if |N+(j)| <= ratio * |tail|
 constexpr int kHistCap = 1 << 16;    // recorded rounds per fixpoint
@@ -1260,15 +1263,15 @@ k_prune_light(Graph g, int fused_reset) {
 // CTA per heavy row (queued by k_prune_light): same compaction with a
 // block-wide scan over tiles of 4 * kPruneThreads slots.
 template <int MODE>
-__global__ void __launch_bounds__(kPruneThreads)
+__global__ void __launch_bounds__(kSymHeavyThreads)
 k_prune_heavy(Graph g, int fused_reset) {
-  __shared__ uint32_t red[kPruneThreads / 32];
+  __shared__ uint32_t red[kSymHeavyThreads / 32];
   __shared__ uint32_t tot_s;
   constexpr int EPT = 4;
-  constexpr int TILE = EPT * kPruneThreads;
+  constexpr int TILE = EPT * kSymHeavyThreads;
   const uint32_t tid = threadIdx.x;
   const int lane = tid & 31, wid = tid >> 5;
-  constexpr int NW = kPruneThreads / 32;
+  constexpr int NW = kSymHeavyThreads / 32;
   uint32_t* __restrict__ S = MODE ? g.S0 : cur_S(g);
   uint32_t* __restrict__ So = other_S(g);
   uint32_t* __restrict__ col = g.col;
@@ -1679,10 +1682,11 @@ k_delta_big(Graph g, Sym y) {
 // the round carries supports, S; pos_of follows every moved edge. Warp per
 // queued row up to kHeavyRow (HEAVY = 0), CTA per longer row (HEAVY = 1).
 template <int HEAVY>
-__global__ void __launch_bounds__(kPruneThreads)
+__global__ void __launch_bounds__(HEAVY ? kSymHeavyThreads : kPruneThreads)
 k_inc_rows(Graph g, Sym y) {
   constexpr int EPT = HEAVY ? 4 : 1;
-  constexpr int NW = kPruneThreads / 32;
+  constexpr int BT = HEAVY ? kSymHeavyThreads : kPruneThreads;
+  constexpr int NW = BT / 32;
   __shared__ uint32_t red[NW];
   __shared__ uint32_t tot_s;
   if (g.st->removed == 0) return;
@@ -1704,7 +1708,7 @@ k_inc_rows(Graph g, Sym y) {
     }
     const uint32_t base = g.row_ptr[u];
     uint32_t write = 0;
-    constexpr uint32_t TILE = HEAVY ? EPT * kPruneThreads : 32;
+    constexpr uint32_t TILE = HEAVY ? EPT * BT : 32;
     for (uint32_t off = 0; off < d; off += TILE) {
       uint32_t c[EPT], sv[EPT], pv[EPT];
       bool keep[EPT];
@@ -1771,9 +1775,6 @@ k_inc_rows(Graph g, Sym y) {
 }
 
 // Symmetric rows that lost an edge drop their dead entries (stable).
-// Heavy rows are few (the hubs), so their kernel runs kSymHeavyThreads-wide
-// CTAs: a row takes 4x fewer dependent tile steps than with 256 threads.
-constexpr int kSymHeavyThreads = 1024;
 template <int HEAVY>
 __global__ void __launch_bounds__(HEAVY ? kSymHeavyThreads : kPruneThreads)
 k_inc_sym(Graph g, Sym y) {
