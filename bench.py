@@ -578,9 +578,11 @@ def run_fixpoint_mode(args):
             kd.engine_join(eng)
     eng.reset()
     hist = eng.run(k)
-    # carried-support rounds on one rank (13 launches per round + 2 + 4);
-    # the partitioned multi-rank loop recomputes (6 per round + 5 publish)
-    launches = (2 + 13 * len(hist) + 2 + 4) if world == 1 else (2 + 6 * len(hist) + 5)
+    # carried-support rounds (13 launches per round + 2 + 4), also across
+    # ranks with the NCCL exchange; the fused peer exchange recomputes every
+    # round (6 per round + 5 publish)
+    fused = world > 1 and args.exchange == "fused"
+    launches = (2 + 6 * len(hist) + 5) if fused else (2 + 13 * len(hist) + 2 + 4)
     flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
     for _ in range(args.warmup):
         eng.reset()

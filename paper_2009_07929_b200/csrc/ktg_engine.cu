@@ -865,6 +865,19 @@ ktg_status enqueue_round(ktg_engine* e, bool graph_mode, cudaGraphConditionalHan
   }
   if (sup1) KTG_CUDA(cudaEventRecord(sup1, s));
   if (e->inc_active) {
+    if (!graph_mode && e->world > 1 && e->h_st->mode == 0 && (e->nccl || e->allreduce)) {
+      // multi-rank carried run: this full pass covered this rank's A22
+      // tasks only; sum the partial supports, then every rank runs the same
+      // deterministic mark / delta / compaction on identical data
+      uint32_t* buf = e->h_st->parity ? L.S1.p : L.S0.p;
+      if (e->nccl) {
+        NcclApi* api = nccl_api();
+        const ncclResult_t r = api->allReduce(buf, buf, L.slots, ncclUint32, ncclSum, e->nccl, e->stream);
+        if (r != ncclSuccess) return fail(KTG_ERR_CUDA, std::string("ncclAllReduce: ") + api->errorString(r));
+      } else if (e->allreduce(buf, L.slots, e->stream, e->allreduce_user) != 0) {
+        return fail(KTG_ERR_CUDA, "allreduce callback failed");
+      }
+    }
     // mark -> [carry: delta] -> compact rows (col, ids, carried S) -> compact
     // symmetric rows -> control (next round's mode, while condition)
     const Sym y = e->sym();
@@ -964,8 +977,8 @@ ktg_status build_graph(ktg_engine* e) {
 // KTG_FLAG_RECOMPUTE keeps the paper's full pass every round.
 bool inc_eligible(const ktg_engine* e) {
   return e->reoriented && e->sym_ready && !flag(e, KTG_FLAG_RECOMPUTE) && !flag(e, KTG_FLAG_NAIVE_SUPPORT) &&
-         e->opt.width_bits == 32 && e->opt.observer == nullptr && e->world == 1 && e->nccl == nullptr &&
-         e->allreduce == nullptr;
+         e->opt.width_bits == 32 && e->opt.observer == nullptr && e->npeer <= 1 &&
+         (e->world == 1 || e->nccl != nullptr || e->allreduce != nullptr);
 }
 
 ktg_status begin_run(ktg_engine* e, uint32_t k, int parity) {

@@ -868,7 +868,8 @@ k_support_a22(Graph g, Sym y, A22 a) {
       s.next = 0;
     }
     __syncthreads();
-    const uint32_t t = s.task;
+    // multi-rank runs: this rank's share of the tasks (t = local * world + rank)
+    const uint32_t t = s.task * g.world + g.rank;
     if (t >= a.ntasks) break;
     const uint2 tk = a.tasks[a.ntasks - 1 - t];  // dense (high-rank) chunks first
     const uint32_t q = tk.x;

@@ -147,3 +147,66 @@ def test_fused_reduce_scatter_two_processes_ipc(port):
             col_e, S_e, hist_e = port.run_fixpoint(g, k, threads=8)
             hist, col, S = out[r][k]
             assert hist == hist_e and np.array_equal(col, col_e) and np.array_equal(S, S_e), (r, k)
+
+
+def test_carried_run_partitioned_virtual_ranks(port):
+    """Multi-rank carried-support run (set_partition): each rank's full
+    passes cover its share of the A22 tasks, the callback sums the partial
+    supports, and every rank runs the same mark / delta / compaction --
+    two engines in two threads on one device, byte-exact against the oracle."""
+    world = 2
+    g = kt.rmat(13, 16, seed=4)
+    engines = [kt.Engine(g) for _ in range(world)]
+    bar = threading.Barrier(world, timeout=120)
+    parts = [None] * world
+    slots = g.total_slots()
+
+    def reducer(r):
+        def cb(d_buf, count, stream, user):
+            try:
+                addr = ctypes.cast(d_buf, ctypes.c_void_p).value
+                host = np.empty(count, np.uint32)
+                truss.device_copy(host.ctypes.data, addr, 4 * count, stream)  # waits for the stream
+                parts[r] = host
+                bar.wait()
+                total = parts[0] + parts[1]
+                bar.wait()
+                truss.device_copy(addr, total.ctypes.data, 4 * count, stream)
+                return 0
+            except Exception:  # pragma: no cover
+                bar.abort()
+                return 1
+        return cb
+
+    for r, e in enumerate(engines):
+        e.set_partition(r, world, allreduce=reducer(r))
+    ks = (3, 6, 10)
+    out = [dict() for _ in range(world)]
+    errs = []
+
+    def body(r):
+        try:
+            for k in ks:
+                engines[r].reset()
+                hist = engines[r].run(k)
+                col, S = engines[r].read()
+                out[r][k] = (hist, col.copy(), S.copy())
+        except Exception as ex:  # pragma: no cover
+            errs.append(ex)
+            bar.abort()
+
+    th = [threading.Thread(target=body, args=(r,)) for r in range(world)]
+    for t in th:
+        t.start()
+    for t in th:
+        t.join()
+    for e in engines:
+        e.close()
+    if errs:
+        raise errs[0]
+    assert slots > 0
+    for k in ks:
+        col_e, S_e, hist_e = port.run_fixpoint(g, k, threads=8)
+        for r in range(world):
+            hist, col, S = out[r][k]
+            assert hist == hist_e and np.array_equal(col, col_e) and np.array_equal(S, S_e), (r, k)
