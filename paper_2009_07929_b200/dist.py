@@ -4,13 +4,15 @@ for rendezvous; the data path is the engine's own ncclAllReduce.
 Two ways the path shards:
   * K sweep   -- K values are independent fixpoints on a replicated graph:
                  split_k_values() hands each rank a share, no collective;
-  * one big fixpoint -- the support tasks are split into work-balanced
-                 ranges; each round every rank either all-reduces its partial
-                 supports (engine_join(): ncclAllReduce, exact u32 sums) or,
-                 fused (engine_join_fused()), sends every increment straight
-                 to the owner rank's buffer over NVLink peer memory during the
-                 support pass and only all-gathers the owned spans; then every
-                 rank runs the same deterministic prune.
+  * one big fixpoint -- every full support pass covers this rank's share
+                 of the tasks (A22 tasks round-robin in carried runs, work-
+                 balanced chunk ranges in recompute runs); the partial
+                 supports are all-reduced (engine_join(): ncclAllReduce,
+                 exact u32 sums) or, fused (engine_join_fused(), recompute
+                 runs), every increment goes straight to the owner rank's
+                 buffer over NVLink peer memory during the support pass and
+                 only the owned spans are all-gathered; then every rank runs
+                 the same deterministic prune / carried rounds.
 """
 from __future__ import annotations
 
