@@ -665,8 +665,9 @@ def run_fixpoint_mode(args):
                        "l2": "512 MiB memset between timed steps; inputs > L2" if slots * 4 > 126e6 else
                              "512 MiB memset between timed steps",
                        "parallelism": (f"edge-partitioned x{world} (" + ("support kernel fused with the reduce-scatter, span "
-                                                                     "all-gather" if args.exchange == "fused" else
-                                                                     "ncclAllReduce of S") + " per round)")
+                                                                     "all-gather per round" if args.exchange == "fused" else
+                                                                     "A22 tasks split by rank, ncclAllReduce of S after each full pass, "
+                                                                     "carried rounds replicated") + ")")
                        if world > 1
                                       else "single"},
             "time_to_fixpoint_ms": ms, "me_per_s": value / 1e6,
