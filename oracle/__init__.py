@@ -183,6 +183,11 @@ class _Ref:
         L.ref_hardware_threads.restype = ctypes.c_int
         L.ref_write_csr_cache.argtypes = [ctypes.c_char_p, _vp, _u32, _vp, _u64]
         L.ref_read_csr_cache.argtypes = [ctypes.c_char_p, _P(_vp)]
+        L.ref_rmat_csr.argtypes = [_u32, _u32, _u64, ctypes.c_double, ctypes.c_double, ctypes.c_double, _vp, _u64,
+                                   ctypes.c_int, _P(_vp)]
+        L.ref_er_csr.argtypes = [_u32, _u64, _u64, ctypes.c_int, _P(_vp)]
+        L.ref_fine_sample.argtypes = [_vp, _u32, _vp, _u64, _vp, _u32, _u32, ctypes.c_int, _P(_u64),
+                                      _P(ctypes.c_double)]
         self.L = L
 
     def _err(self, rc):
@@ -209,6 +214,31 @@ class _Ref:
         h = _vp()
         self._err(self.L.ref_canonicalize_csr(_p(a), a.shape[0], ctypes.byref(h)))
         return self._csr(h)
+
+    def rmat(self, scale, edgefactor=16, seed=42, extra_pairs=None, fast=True, a=0.57, b=0.19, c=0.19):
+        """SURVEY §8(d) R-MAT (+ optional extra label pairs, e.g. planted
+        cliques), canonicalized by the reference canonicalize (fast=False) or
+        its parallel restatement (fast=True), built by the reference build_csr."""
+        ex = np.zeros((0, 2), np.uint64) if extra_pairs is None else np.ascontiguousarray(extra_pairs, np.uint64)
+        h = _vp()
+        self._err(self.L.ref_rmat_csr(scale, edgefactor, seed, a, b, c, _p(ex), ex.shape[0], int(fast),
+                                      ctypes.byref(h)))
+        return self._csr(h)
+
+    def erdos_renyi(self, log_n, m, seed=42, fast=True):
+        h = _vp()
+        self._err(self.L.ref_er_csr(log_n, m, seed, int(fast), ctypes.byref(h)))
+        return self._csr(h)
+
+    def fine_sample(self, g, stride, phase, threads, supports=None):
+        """support.cpp:115-127 (reference intersect_tails per slot) over the
+        256-slot chunks c % stride == phase. Returns (triangles, S, ms)."""
+        S = np.zeros(g.total_slots(), np.uint32) if supports is None else supports
+        t, ms = _u64(), ctypes.c_double()
+        self._err(self.L.ref_fine_sample(_p(_u32a(g.row_ptr)), g.num_vertices, _p(_u32a(g.col_idx)),
+                                         g.total_slots(), _p(S), stride, phase, threads, ctypes.byref(t),
+                                         ctypes.byref(ms)))
+        return int(t.value), S, ms.value
 
     def compute_supports(self, g, strategy=2, threads=1, width16=False, supports=None):
         S = np.zeros(g.total_slots(), np.uint32) if supports is None else supports
@@ -301,6 +331,31 @@ class _Ref:
 
 _port = None
 _ref = None
+
+
+def clique_members(n_labels, c, seed):
+    """c distinct labels of [0, n_labels): the first c positions of a partial
+    Fisher-Yates shuffle driven by numpy's MT19937(seed) (the planted-clique
+    spec of BASELINE configs[4], restated independently of the product)."""
+    rng = np.random.Generator(np.random.MT19937(seed))
+    draws = rng.integers(0, np.arange(n_labels, n_labels - c, -1, dtype=np.int64), dtype=np.int64)
+    swapped = {}
+    out = np.empty(c, np.uint64)
+    for i in range(c):
+        j = i + int(draws[i])
+        out[i] = swapped.get(j, j)
+        swapped[j] = swapped.get(i, i)
+    return out
+
+
+def clique_pairs(n_labels, sizes, seed):
+    """Every pair of each planted clique; clique i uses seed + i."""
+    parts = []
+    for i, c in enumerate(sizes):
+        mem = clique_members(n_labels, int(c), seed + i)
+        iu, ju = np.triu_indices(len(mem), 1)
+        parts.append(np.stack([mem[iu], mem[ju]], axis=1))
+    return np.concatenate(parts).astype(np.uint64)
 
 
 def port() -> _Port:

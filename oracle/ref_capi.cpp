@@ -13,6 +13,15 @@
 //   ref_canonicalize_csr -> ktruss::canonicalize + build_csr (edge_list.hpp:53, csr.hpp:27)
 //   ref_random_graph_csr -> ktruss::oracle::random_graph + build_csr (oracle.hpp:38)
 //   ref_oracle_*         -> ktruss::oracle::{edge_supports,ktruss_edges,kmax,triangle_count}
+//   ref_rmat_csr / ref_er_csr -> the SURVEY §8(d) synthetic generators (restated
+//                           here, independent of the product's graph_host.cpp),
+//                           then either the reference canonicalize + build_csr
+//                           (fast=0) or a parallel restatement of canonicalize
+//                           feeding the reference build_csr (fast=1; pinned
+//                           byte-equal to fast=0 by tests/test_oracle.py and the
+//                           s20/s24 digests in tests/golden/large_ref.json).
+#include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cstdint>
 #include <cstring>
@@ -21,6 +30,8 @@
 #include <vector>
 
 #include <fstream>
+#include <parallel/algorithm>
+#include <random>
 #include <sstream>
 
 #include "ktruss/bench.hpp"
@@ -319,5 +330,163 @@ double ref_millions_of_edges_per_second(std::uint64_t edges, double ms) {
 }
 
 int ref_hardware_threads() { return hardware_threads(); }
+
+}  // extern "C"
+
+// ---- synthetic inputs -------------------------------------
+namespace {
+
+double u01(std::mt19937_64& g) { return static_cast<double>(g() >> 11) * 0x1.0p-53; }
+
+// R-MAT raw pairs, Graph500 quadrant draw per level, then the explicit
+// Fisher-Yates relabel driven by mt19937_64(seed ^ 0xABCDEF).
+std::vector<RawEdge> rmat_raw(std::uint32_t scale, std::uint32_t ef, std::uint64_t seed, double a, double b,
+                              double c) {
+  const std::uint64_t N = std::uint64_t{1} << scale, m = N * ef;
+  std::vector<RawEdge> raw(m);
+  std::mt19937_64 g(seed);
+  for (auto& e : raw) {
+    std::uint64_t u = 0, v = 0;
+    for (std::uint32_t l = 0; l < scale; ++l) {
+      const double x = u01(g);
+      const std::uint64_t bu = x < a + b ? 0 : 1;
+      const std::uint64_t bv = (x < a || (x >= a + b && x < a + b + c)) ? 0 : 1;
+      u = (u << 1) | bu;
+      v = (v << 1) | bv;
+    }
+    e = {u, v};
+  }
+  std::vector<std::uint64_t> perm(N);
+  for (std::uint64_t i = 0; i < N; ++i) perm[i] = i;
+  std::mt19937_64 g2(seed ^ 0xABCDEFull);
+  for (std::uint64_t i = N - 1; i >= 1; --i) std::swap(perm[i], perm[g2() % (i + 1)]);
+#pragma omp parallel for schedule(static)
+  for (std::uint64_t i = 0; i < m; ++i) raw[i] = {perm[raw[i].first], perm[raw[i].second]};
+  return raw;
+}
+
+// Parallel restatement of canonicalize (edge_list.cpp:62-103) for labels
+// below `bound`: dense rank of the labels seen in non-loop pairs (= sorted
+// unique + lower_bound + 1), orient u<v, sort, unique. Same EdgeList.
+EdgeList canonicalize_fast(const std::vector<RawEdge>& raw, std::uint64_t bound) {
+  std::vector<std::uint32_t> seen(bound, 0);
+#pragma omp parallel for schedule(static)
+  for (std::uint64_t i = 0; i < raw.size(); ++i) {
+    if (raw[i].first == raw[i].second) continue;
+    __atomic_store_n(&seen[raw[i].first], 1u, __ATOMIC_RELAXED);
+    __atomic_store_n(&seen[raw[i].second], 1u, __ATOMIC_RELAXED);
+  }
+  EdgeList el;
+  el.original_ids.push_back(0);
+  std::uint32_t n = 0;
+  for (std::uint64_t l = 0; l < bound; ++l) {
+    if (seen[l]) {
+      seen[l] = ++n;
+      el.original_ids.push_back(l);
+    }
+  }
+  if (n == 0) throw EmptyGraphError("no edges survive canonicalization");
+  el.num_vertices = n;
+  std::vector<std::uint64_t> keys(raw.size());
+#pragma omp parallel for schedule(static)
+  for (std::uint64_t i = 0; i < raw.size(); ++i) {
+    const auto [x, y] = raw[i];
+    const std::uint64_t u = seen[x], v = seen[y];
+    keys[i] = x == y ? ~std::uint64_t{0} : (u < v ? (u << 32 | v) : (v << 32 | u));
+  }
+  __gnu_parallel::sort(keys.begin(), keys.end());
+  keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+  if (!keys.empty() && keys.back() == ~std::uint64_t{0}) keys.pop_back();
+  el.edges.resize(keys.size());
+#pragma omp parallel for schedule(static)
+  for (std::uint64_t i = 0; i < keys.size(); ++i)
+    el.edges[i] = {static_cast<std::uint32_t>(keys[i] >> 32), static_cast<std::uint32_t>(keys[i])};
+  return el;
+}
+
+CsrOut* csr_of(std::vector<RawEdge>& raw, std::uint64_t bound, int fast) {
+  auto* c = new CsrOut;
+  try {
+    c->csr = build_csr(fast ? canonicalize_fast(raw, bound) : canonicalize(raw));
+  } catch (...) {
+    delete c;
+    throw;
+  }
+  return c;
+}
+
+}  // namespace
+
+extern "C" {
+
+// R-MAT(scale, ef, seed; a,b,c) plus `n_extra` extra label pairs (planted
+// cliques), canonicalized and built into the reference CSR.
+int ref_rmat_csr(std::uint32_t scale, std::uint32_t ef, std::uint64_t seed, double a, double b, double c,
+                 const std::uint64_t* extra, std::uint64_t n_extra, int fast, void** out) {
+  try {
+    std::vector<RawEdge> raw = rmat_raw(scale, ef, seed, a, b, c);
+    const std::uint64_t base = raw.size();
+    raw.resize(base + n_extra);
+    for (std::uint64_t i = 0; i < n_extra; ++i) raw[base + i] = {extra[2 * i], extra[2 * i + 1]};
+    *out = csr_of(raw, std::uint64_t{1} << scale, fast);
+    return 0;
+  } catch (const std::exception& e) {
+    return code_of(e);
+  }
+}
+
+// Erdos-Renyi: m draws of (g() % 2^log_n, g() % 2^log_n) from mt19937_64(seed).
+int ref_er_csr(std::uint32_t log_n, std::uint64_t m, std::uint64_t seed, int fast, void** out) {
+  try {
+    const std::uint64_t N = std::uint64_t{1} << log_n;
+    std::vector<RawEdge> raw(m);
+    std::mt19937_64 g(seed);
+    for (auto& e : raw) {
+      const std::uint64_t x = g() % N;
+      e = {x, g() % N};
+    }
+    *out = csr_of(raw, N, fast);
+    return 0;
+  } catch (const std::exception& e) {
+    return code_of(e);
+  }
+}
+
+// Fine branch of compute_supports (support.cpp:115-127) restricted to the
+// 256-slot chunks c (the omp dynamic,256 grain) with c % stride == phase, each
+// slot through the reference's own intersect_tails. A bounded sample of one
+// support pass for bench.py's cpu_baseline; supports accumulate into S.
+// *elapsed_ms brackets the task loop only.
+int ref_fine_sample(const std::uint32_t* row_ptr, std::uint32_t n, const std::uint32_t* col,
+                    std::uint64_t slots, std::uint32_t* supports, std::uint32_t stride, std::uint32_t phase,
+                    int threads, std::uint64_t* triangles, double* elapsed_ms) {
+  try {
+    if (threads < 1 || stride < 1) throw InvalidParameterError("thread count must be >= 1");
+    const ZeroTerminatedCsr g = make_csr(row_ptr, n, col, slots);
+    SupportArray s;
+    s.counts.assign(supports, supports + slots);
+    const std::uint64_t chunks = (slots + 255) / 256;
+    std::uint64_t tri = 0;
+    const auto t0 = std::chrono::steady_clock::now();
+#pragma omp parallel for schedule(dynamic, 1) num_threads(threads) reduction(+ : tri)
+    for (std::uint64_t c = phase; c < chunks; c += stride) {
+      const std::uint64_t end = std::min<std::uint64_t>(slots, (c + 1) * 256);
+      for (std::uint64_t slot = c * 256; slot < end; ++slot) {
+        const std::uint32_t pred = g.col_idx[slot];
+        if (pred == 0) continue;
+        const std::uint32_t found = intersect_tails(g, static_cast<std::uint32_t>(slot), pred, s);
+        if (found != 0) std::atomic_ref<std::uint32_t>(s.counts[slot]).fetch_add(found, std::memory_order_relaxed);
+        tri += found;
+      }
+    }
+    const auto t1 = std::chrono::steady_clock::now();
+    if (elapsed_ms) *elapsed_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    *triangles = tri;
+    std::memcpy(supports, s.counts.data(), slots * 4);
+    return 0;
+  } catch (const std::exception& e) {
+    return code_of(e);
+  }
+}
 
 }  // extern "C"

@@ -178,6 +178,9 @@ struct ktg_engine {
   DBuf<uint32_t> a22_pe, a22_off, a22_jfirst, a22_cnt;
   DBuf<uint2> a22_tasks, a22_pin;
   uint32_t a22_ntasks = 0;
+  // multi-rank full passes: per-task work (k_support_a22<true>) and its
+  // exclusive prefix (ntasks + 1 entries; cost[ntasks] stays 0)
+  DBuf<unsigned long long> a22_cost, a22_pre;
   bool a22_ready = false;
   bool a22_off_env = false;   // KTG_SUPPORT=chunked: keep k_support_chunked in carried runs
   int a22_grid = 0;
@@ -294,6 +297,8 @@ struct ktg_engine {
     sdirty.release();
     rq.release();
     a22_tasks.release();
+    a22_cost.release();
+    a22_pre.release();
     a22_pin.release();
     sym_ready = false;
     a22_ready = false;
@@ -360,7 +365,7 @@ ktg_status engine_init(const ktg_options* opt, ktg_engine* e) {
   e->heavy_grid = 2 * e->num_sms;
   e->a22_smem = 0;  // static shared memory (sizeof(A22Smem) < 48 KB)
   int per_sm_a = 0;
-  KTG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_a, k_support_a22, kSupportThreads, e->a22_smem));
+  KTG_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm_a, k_support_a22<false>, kSupportThreads, e->a22_smem));
   e->a22_grid = std::max(1, per_sm_a) * e->num_sms;
   if (const char* v = getenv("KTG_SUPPORT")) e->a22_off_env = std::string(v) == "chunked";
   return KTG_OK;
@@ -563,6 +568,14 @@ ktg_status build_a22(ktg_engine* e) {
   k_a22_fill<<<(Q + 255) / 256, 256, 0, s>>>(e->a22_cnt.p, Q, e->a22_tasks.p);
   KTG_CUDA(cudaGetLastError());
   e->a22_ntasks = total;
+  // the multi-rank split's buffers (and scan scratch) exist before any
+  // fixpoint is captured into a graph
+  KTG_TRY(e->a22_cost.ensure((size_t)total + 1));
+  KTG_TRY(e->a22_pre.ensure((size_t)total + 1));
+  KTG_CUDA(cudaMemsetAsync(e->a22_cost.p, 0, ((size_t)total + 1) * 8, s));
+  tmp = 0;
+  KTG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, e->a22_cost.p, e->a22_pre.p, (int)total + 1, s));
+  KTG_TRY(e->cub_tmp.ensure(tmp));
   e->a22_ready = true;
   return KTG_OK;
 }
@@ -852,7 +865,16 @@ ktg_status enqueue_round(ktg_engine* e, bool graph_mode, cudaGraphConditionalHan
   if (sup0) KTG_CUDA(cudaEventRecord(sup0, s));
   if (a22) {
     A22 a{e->a22_pe.p, e->a22_pin.p, e->a22_off.p, e->a22_jfirst.p, e->a22_tasks.p, e->a22_ntasks};
-    k_support_a22<<<e->a22_grid, kSupportThreads, e->a22_smem, s>>>(g, e->sym(), a);
+    if (e->world > 1) {
+      // work-balanced split of this full pass across ranks: exact per-task
+      // work on the current graph, prefix sum, this rank's contiguous range
+      k_support_a22<true><<<e->a22_grid, kSupportThreads, e->a22_smem, s>>>(g, e->sym(), a, e->a22_cost.p);
+      size_t tmp = e->cub_tmp.cap;
+      KTG_CUDA(cub::DeviceScan::ExclusiveSum(e->cub_tmp.p, tmp, e->a22_cost.p, e->a22_pre.p,
+                                             (int)e->a22_ntasks + 1, s));
+      k_a22_split<<<1, 1, 0, s>>>(e->d_st, e->a22_pre.p, e->a22_ntasks, e->rank_id, e->world);
+    }
+    k_support_a22<false><<<e->a22_grid, kSupportThreads, e->a22_smem, s>>>(g, e->sym(), a, nullptr);
   } else if (flag(e, KTG_FLAG_NAIVE_SUPPORT)) {
     k_support_naive<<<4 * e->num_sms, 256, 0, s>>>(g);
   } else {
@@ -1132,6 +1154,15 @@ ktg_status copy_hist(ktg_engine* e, uint64_t* hist, uint32_t cap, uint32_t* iter
 // (ktg_compute_supports accumulates like the reference).
 ktg_status support_pass(ktg_engine* e, int parity, uint64_t* triangles, bool max_support, bool add_to_caller) {
   Layout& L = e->act();
+  // A standalone pass (compute_supports, the kmax_search bound) is never
+  // partitioned: every rank of a partitioned engine computes all tasks, so
+  // T, max S and S are whole-graph values on every rank without an exchange.
+  struct Solo {
+    ktg_engine* e;
+    uint32_t rank, world, npeer;
+    ~Solo() { e->rank_id = rank, e->world = world, e->npeer = npeer; }
+  } solo{e, e->rank_id, e->world, e->npeer};
+  e->rank_id = 0, e->world = 1, e->npeer = 0;
   Graph g = e->graph_of(L);
   e->inc_active = false;
   k_begin<<<1, 1, 0, e->stream>>>(e->d_st, 0, e->opt.width_bits == 16 ? 1 : 0, parity, 0u, e->delta_ratio, e->delta_ratio0);
@@ -1512,10 +1543,29 @@ ktg_status ktg_engine_extract(ktg_engine* e, uint32_t* out_u, uint32_t* out_v, u
   return extract(e, out_u, out_v, out_support, edge_cap, num_edges);
 }
 
+// Exactly one exchange is active per engine: installing one drops the others
+// (an NCCL communicator, the fused peer exchange, the allreduce callback).
+static void drop_exchanges(ktg_engine* e, bool nccl, bool peers, bool cb) {
+  if (nccl && e->nccl) {
+    if (NcclApi* api = nccl_api()) api->commDestroy(e->nccl);
+    e->nccl = nullptr;
+  }
+  if (peers) {
+    e->npeer = 0;
+    e->peer_cb = nullptr;
+    e->peer_user = nullptr;
+  }
+  if (cb) {
+    e->allreduce = nullptr;
+    e->allreduce_user = nullptr;
+  }
+}
+
 ktg_status ktg_engine_set_partition(ktg_engine* e, uint32_t rank, uint32_t world, ktg_allreduce_cb allreduce,
                                     void* user) {
   if (world == 0 || rank >= world) return fail(KTG_ERR_INVALID_PARAMETER, "rank must be < world");
   if (world > 1 && !allreduce) return fail(KTG_ERR_INVALID_PARAMETER, "world > 1 needs an allreduce callback");
+  drop_exchanges(e, true, true, true);
   e->rank_id = rank;
   e->world = world;
   e->allreduce = allreduce;
@@ -1553,6 +1603,7 @@ ktg_status ktg_engine_set_peers(ktg_engine* e, uint32_t rank, uint32_t world, ui
     return fail(KTG_ERR_INVALID_PARAMETER, "world > 1 needs peer buffers and an exchange callback");
   if (world > 1 && (peer_s0[rank] != L.S0.p || peer_s1[rank] != L.S1.p))
     return fail(KTG_ERR_INVALID_PARAMETER, "peer tables must hold this engine's own support buffers at its rank");
+  drop_exchanges(e, true, true, false);
   e->rank_id = rank;
   e->world = world;
   e->allreduce = nullptr;
@@ -1604,8 +1655,7 @@ ktg_status ktg_engine_set_nccl(ktg_engine* e, uint32_t rank, uint32_t world, con
   if (world == 0 || rank >= world) return fail(KTG_ERR_INVALID_PARAMETER, "rank must be < world");
   NcclApi* api = nccl_api();
   if (!api) return fail(KTG_ERR_CUDA, "libnccl.so.2 not loadable");
-  if (e->nccl) api->commDestroy(e->nccl);
-  e->nccl = nullptr;
+  drop_exchanges(e, true, true, true);
   ncclUniqueId id;
   std::memcpy(&id, unique_id, sizeof(id));
   KTG_CUDA(cudaSetDevice(e->device));

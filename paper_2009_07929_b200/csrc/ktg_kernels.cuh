@@ -73,6 +73,7 @@ struct DevState {
   double delta_ratio0;               // the same for round 0 of a run from the pristine graph
   unsigned int dq_lo, dq_hi;         // this rank's diagonal support tasks: chunks [dq_lo, dq_hi)
   unsigned long long rq_cap;         // delta piece queue capacity (a round that could exceed it recomputes)
+  unsigned int a22_lo, a22_hi;       // this rank's A22 tasks [lo, hi) of the current full pass (world > 1)
 };
 
 struct Graph {
@@ -807,6 +808,10 @@ k_support_chunked(Graph g) {
 #define KTG_A22_UNROLL 4
 #endif
 constexpr int kA22Batch = 256;
+#ifndef KTG_A22_GROUP
+#define KTG_A22_GROUP 8
+#endif
+constexpr int kA22Group = KTG_A22_GROUP;   // batches of one chunk per task (staged once)
 constexpr int kA22TableBits = 11;          // 2048 slots for <= 512 entries (load <= 0.25)
 constexpr int kA22Strip = 256;             // flat tail elements a warp takes per grab
 constexpr int kA22Table = 1 << kA22TableBits;
@@ -847,8 +852,15 @@ __device__ __forceinline__ uint32_t a22_mix(uint32_t v, uint32_t te) {
 __device__ __forceinline__ uint32_t a22_slot(uint32_t h) { return h >> (32 - kA22TableBits); }
 __device__ __forceinline__ uint32_t a22_fbit(uint32_t h) { return (h ^ (h >> 15)) & (kA22FiltWords * 32 - 1); }
 
-__global__ void __launch_bounds__(kSupportThreads)
-k_support_a22(Graph g, Sym y, A22 a) {
+// COST = true (multi-rank runs, before every full pass): steps 1-2 only, over
+// all tasks; cost[t] = the task's flattened tail work W, the weights of the
+// work-balanced split of the tasks across ranks (k_a22_split).
+#ifndef KTG_A22_MINB
+#define KTG_A22_MINB 6
+#endif
+template <bool COST>
+__global__ void __launch_bounds__(kSupportThreads, KTG_A22_MINB)
+k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ cost) {
   if (g.st->mode) return;  // supports carried this round
   // static (not dynamic) shared memory: constant-offset LDS addressing
   __shared__ __align__(16) A22Smem s;
@@ -860,17 +872,18 @@ k_support_a22(Graph g, Sym y, A22 a) {
   const uint32_t* __restrict__ col = g.col;
   const uint32_t h0 = g.st->h0;
   const bool pristine = g.st->pristine;
+  // multi-rank runs: this rank's contiguous, work-balanced range of tasks
+  const uint32_t t_lo = (g.world > 1 && !COST) ? g.st->a22_lo : 0u;
+  const uint32_t t_hi = (g.world > 1 && !COST) ? g.st->a22_hi : a.ntasks;
+  unsigned long long task_w = 0;
   unsigned long long tri_local = 0;
 
   for (;;) {
-    if (tid == 0) {
-      s.task = atomicAdd(&g.st->task_next, 1u);
-      s.next = 0;
-    }
+    if (tid == 0) s.task = atomicAdd(&g.st->task_next, 1u);
     __syncthreads();
-    // multi-rank runs: this rank's share of the tasks (t = local * world + rank)
-    const uint32_t t = s.task * g.world + g.rank;
-    if (t >= a.ntasks) break;
+    const uint32_t t = t_lo + s.task;
+    if (t >= t_hi) break;
+    task_w = 0;
     const uint2 tk = a.tasks[a.ntasks - 1 - t];  // dense (high-rank) chunks first
     const uint32_t q = tk.x;
     const uint64_t a0 = (uint64_t)q * kChunk;
@@ -878,9 +891,9 @@ k_support_a22(Graph g, Sym y, A22 a) {
     const uint32_t jf = a.jfirst[q], jl = g.chunk_row[q];
     const uint32_t nrows = jl - jf + 1;
 
-    // 1. rows of the chunk (live run inside the chunk, in-list offsets) and
-    //    the batch's pivot descriptors, before anything is staged: batches
-    //    whose pivots are all dead cost only this
+    // 1. rows of the chunk (live run inside the chunk, in-list offsets),
+    //    once per task: a task is up to kA22Group consecutive batches of the
+    //    same chunk, so the chunk is staged once for all of them
     for (uint32_t r = tid; r <= nrows; r += kSupportThreads) {
       const uint32_t j = jf + r;
       s.roff[r] = a.pin_off[j];
@@ -891,183 +904,210 @@ k_support_a22(Graph g, Sym y, A22 a) {
       }
     }
     __syncthreads();
+    const uint32_t kbeg = s.roff[0], kend = s.roff[nrows];
+    const uint32_t ylim = min(tk.y + (uint32_t)kA22Group, (kend - kbeg + kA22Batch - 1) / kA22Batch);
+    bool staged = false;  // block-uniform
 
-    // 2. pivot descriptors of this batch: slot, tail (clipped to the run's
-    //    value range when j's row continues outside the chunk)
-    const uint32_t k0 = s.roff[0] + tk.y * kA22Batch;
-    const uint32_t k1 = min(k0 + kA22Batch, s.roff[nrows]);
-    uint32_t cost = 0;
-    s.cntP[tid] = 0;
-    if (k0 + tid < k1) {
-      const uint32_t k = k0 + tid;
-      // row of pivot k: last r with roff[r] <= k
-      uint32_t lo = 0, hi = nrows;
-      while (hi - lo > 1) {
-        const uint32_t mid = (lo + hi) >> 1;
-        if (s.roff[mid] <= k) lo = mid; else hi = mid;
-      }
-      const uint32_t run = s.rte[lo];
-      bool live = false;
-      uint32_t ps = 0, i = 0;
-      if (run != 0xffffffffu) {
-        if (pristine) {  // static {slot, row}: no dead / pos_of / erow gathers
-          const uint2 pv = a.pin_p[k];
-          ps = pv.x, i = pv.y, live = true;
-        } else {
-          const uint32_t id = a.pe[k];
-          live = !y.dead[id];
-          if (live) ps = y.pos_of[id], i = y.erow[id];
+    for (uint32_t yb = tk.y; yb < ylim; ++yb) {
+      // 2. pivot descriptors of this batch: slot, tail (clipped to the run's
+      //    value range when j's row continues outside the chunk)
+      const uint32_t k0 = kbeg + yb * kA22Batch;
+      const uint32_t k1 = min(k0 + kA22Batch, kend);
+      uint32_t cost = 0;
+      s.cntP[tid] = 0;
+      if (tid == 0) s.next = 0;
+      if (k0 + tid < k1) {
+        const uint32_t k = k0 + tid;
+        // row of pivot k: last r with roff[r] <= k
+        uint32_t lo = 0, hi = nrows;
+        while (hi - lo > 1) {
+          const uint32_t mid = (lo + hi) >> 1;
+          if (s.roff[mid] <= k) lo = mid; else hi = mid;
+        }
+        const uint32_t run = s.rte[lo];
+        bool live = false;
+        uint32_t ps = 0, i = 0;
+        if (run != 0xffffffffu) {
+          if (pristine) {  // static {slot, row}: no dead / pos_of / erow gathers
+            const uint2 pv = a.pin_p[k];
+            ps = pv.x, i = pv.y, live = true;
+          } else {
+            const uint32_t id = a.pe[k];
+            live = !y.dead[id];
+            if (live) ps = y.pos_of[id], i = y.erow[id];
+          }
+        }
+        if (live) {
+          const uint32_t iend = g.row_ptr[i] + g.deg[i];
+          uint32_t tlo = ps + 1, thi = iend;
+          const uint32_t tb = run >> 16, te = run & 0xffffu;
+          const uint32_t j = jf + lo;
+          const uint64_t rb = g.row_ptr[j];
+          if (rb < a0 || rb + g.deg[j] > a0 + alen) {  // partial run: clip the tail
+            tlo = lb_global(col, tlo, thi, col[a0 + tb]);
+            thi = lb_global(col, tlo, thi, col[a0 + te - 1] + 1);
+          }
+          if (thi > tlo) {
+            cost = thi - tlo;
+            s.ps[tid] = ps;
+            s.plo[tid] = tlo;
+            s.prun[tid] = run;
+          }
         }
       }
-      if (live) {
-        const uint32_t iend = g.row_ptr[i] + g.deg[i];
-        uint32_t tlo = ps + 1, thi = iend;
-        const uint32_t tb = run >> 16, te = run & 0xffffu;
-        const uint32_t j = jf + lo;
-        const uint64_t rb = g.row_ptr[j];
-        if (rb < a0 || rb + g.deg[j] > a0 + alen) {  // partial run: clip the tail
-          tlo = lb_global(col, tlo, thi, col[a0 + tb]);
-          thi = lb_global(col, tlo, thi, col[a0 + te - 1] + 1);
-        }
-        if (thi > tlo) {
-          cost = thi - tlo;
-          s.ps[tid] = ps;
-          s.plo[tid] = tlo;
-          s.prun[tid] = run;
-        }
+      uint32_t W;
+      const uint32_t run0 = block_exscan(cost, s.red, &W);
+      s.pref[tid] = run0;
+      if (tid == 0) s.pref[kA22Batch] = W;
+      if (COST) {
+        task_w += W;
+        __syncthreads();  // s.red / s.pref reused by the next batch
+        continue;
       }
-    }
-    uint32_t W;
-    const uint32_t run0 = block_exscan(cost, s.red, &W);
-    s.pref[tid] = run0;
-    if (tid == 0) s.pref[kA22Batch] = W;
-    if (W == 0) continue;  // no live pivot reaches this chunk (uniform; nothing staged yet)
+      if (W == 0) continue;  // no live pivot of this batch reaches the chunk (uniform)
 
-    // 3. stage the chunk, next zeros, (value, run end) hash -- as k_support_chunked
-    for (uint32_t b = tid; b < (uint32_t)kA22Table; b += kSupportThreads) s.tab[b] = make_uint2(0, 0);
-    for (uint32_t b = tid; b < (uint32_t)kA22FiltWords; b += kSupportThreads) s.filt[b] = 0;
-    uint32_t first_zero = 0xffffffffu;
+      // 3. first non-empty batch: stage the chunk, next zeros, (value, run
+      //    end) hash -- as k_support_chunked
+      if (!staged) {
+        staged = true;
+        for (uint32_t b = tid; b < (uint32_t)kA22Table; b += kSupportThreads) s.tab[b] = make_uint2(0, 0);
+        for (uint32_t b = tid; b < (uint32_t)kA22FiltWords; b += kSupportThreads) s.filt[b] = 0;
+        uint32_t first_zero = 0xffffffffu;
 #pragma unroll
-    for (int e = 0; e < EPT; ++e) {
-      const uint32_t x = tid * EPT + e;
-      const uint32_t v = x < alen ? col[a0 + x] : 0u;
-      s.A[x] = v;
-      s.cntA[x] = 0;
-      if (v == 0 && x < alen && first_zero == 0xffffffffu) first_zero = x;
-    }
-    {
-      uint32_t m = first_zero;
+        for (int e = 0; e < EPT; ++e) {
+          const uint32_t x = tid * EPT + e;
+          const uint32_t v = x < alen ? col[a0 + x] : 0u;
+          s.A[x] = v;
+          s.cntA[x] = 0;
+          if (v == 0 && x < alen && first_zero == 0xffffffffu) first_zero = x;
+        }
+        uint32_t m = first_zero;
 #pragma unroll
-      for (int o = 1; o < 32; o <<= 1) {
-        const uint32_t v = __shfl_down_sync(0xffffffffu, m, o);
-        if (lane + o < 32) m = min(m, v);
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t v = __shfl_down_sync(0xffffffffu, m, o);
+          if (lane + o < 32) m = min(m, v);
+        }
+        if (lane == 0) s.red[wid] = m;
+        __syncthreads();
+        uint32_t carry = 0xffffffffu;
+        for (int w = wid + 1; w < NW; ++w) carry = min(carry, s.red[w]);
+        const uint32_t incl_next = __shfl_down_sync(0xffffffffu, m, 1);
+        if (lane < 31) carry = min(carry, incl_next);
+        uint32_t cur = min(carry, alen);
+#pragma unroll
+        for (int e = EPT - 1; e >= 0; --e) {
+          const uint32_t x = tid * EPT + e;
+          const uint32_t v = s.A[x];
+          if (x < alen && v == 0) cur = x;
+          if (v != 0) {  // claim the first free slot from home (values are >= 1)
+            const uint32_t hh = a22_mix(v, cur);
+            const uint32_t fb = a22_fbit(hh);
+            atomicOr(&s.filt[fb >> 5], 1u << (fb & 31));
+            uint32_t h = a22_slot(hh);
+            while (atomicCAS(&s.tab[h].x, 0u, v) != 0u) h = (h + 1) & (kA22Table - 1);
+            s.tab[h].y = x;
+          }
+        }
       }
-      if (lane == 0) s.red[wid] = m;
       __syncthreads();
-      uint32_t carry = 0xffffffffu;
-      for (int w = wid + 1; w < NW; ++w) carry = min(carry, s.red[w]);
-      const uint32_t incl_next = __shfl_down_sync(0xffffffffu, m, 1);
-      if (lane < 31) carry = min(carry, incl_next);
-      uint32_t cur = min(carry, alen);
-#pragma unroll
-      for (int e = EPT - 1; e >= 0; --e) {
-        const uint32_t x = tid * EPT + e;
-        const uint32_t v = s.A[x];
-        if (x < alen && v == 0) cur = x;
-        if (v != 0) {  // claim the first free slot from home (values are >= 1)
-          const uint32_t hh = a22_mix(v, cur);
-          const uint32_t fb = a22_fbit(hh);
-          atomicOr(&s.filt[fb >> 5], 1u << (fb & 31));
-          uint32_t h = a22_slot(hh);
-          while (atomicCAS(&s.tab[h].x, 0u, v) != 0u) h = (h + 1) & (kA22Table - 1);
-          s.tab[h].y = x;
-        }
-      }
-    }
-    __syncthreads();
 
-    // 4. flattened tail elements, strips grabbed dynamically by warps
-    uint32_t tri_task = 0;
-    for (;;) {
-      uint32_t base = 0;
-      if (lane == 0) base = atomicAdd(&s.next, (uint32_t)kA22Strip);
-      base = __shfl_sync(0xffffffffu, base, 0);
-      if (base >= W) break;
-      const uint32_t lim = min(base + (uint32_t)kA22Strip, W);
-      // pivot holding base: p = #{q in [1, kA22Batch) : pref[q] <= base}
-      // (pref ascends), two ballots over groups of 8 instead of a search
-      static_assert(kA22Batch == 256, "two-level ballot assumes 32 groups of 8");
-      uint32_t p;
-      {
-        const uint32_t g = __popc(__ballot_sync(0xffffffffu, lane < 31 && s.pref[8 * (lane + 1)] <= base));
-        const uint32_t c2 = __popc(__ballot_sync(0xffffffffu, lane < 7 && s.pref[8 * g + 1 + lane] <= base));
-        p = 8 * g + c2;
-      }
-      uint32_t pe_ = s.pref[p + 1], pb = s.pref[p], plo = s.plo[p], prun = s.prun[p];
-      // (value, run) lookup of tail element c of pivot pp: the value may also
-      // sit in other rows' runs
-      auto probe = [&](uint32_t c, uint32_t slot, uint32_t run, uint32_t pp) {
-        const uint32_t tb = run >> 16, te = run & 0xffffu;
-        const uint32_t hh = a22_mix(c, te);
-        const uint32_t fb = a22_fbit(hh);
-        if (s.filt[fb >> 5] & (1u << (fb & 31))) {
-          uint32_t x = kChunk;
-          for (uint32_t h = a22_slot(hh);; h = (h + 1) & (kA22Table - 1)) {
-            const uint2 e = s.tab[h];
-            if (e.x == 0) break;
-            if (e.x == c && e.y - tb < te - tb) {
-              x = e.y;
-              break;
+      // 4. flattened tail elements, strips grabbed dynamically by warps
+      uint32_t tri_task = 0;
+      // pivot counts accumulate per lane while its pivot stays the same (a
+      // lane's pivot index only grows) and go to smem once per change
+      uint32_t accP = 0, accN = 0;
+      for (;;) {
+        uint32_t base = 0;
+        if (lane == 0) base = atomicAdd(&s.next, (uint32_t)kA22Strip);
+        base = __shfl_sync(0xffffffffu, base, 0);
+        if (base >= W) break;
+        const uint32_t lim = min(base + (uint32_t)kA22Strip, W);
+        // pivot holding base: p = #{q in [1, kA22Batch) : pref[q] <= base}
+        // (pref ascends), two ballots over groups of 8 instead of a search
+        static_assert(kA22Batch == 256, "two-level ballot assumes 32 groups of 8");
+        uint32_t p;
+        {
+          const uint32_t g8 = __popc(__ballot_sync(0xffffffffu, lane < 31 && s.pref[8 * (lane + 1)] <= base));
+          const uint32_t c2 = __popc(__ballot_sync(0xffffffffu, lane < 7 && s.pref[8 * g8 + 1 + lane] <= base));
+          p = 8 * g8 + c2;
+        }
+        uint32_t pe_ = s.pref[p + 1], pb = s.pref[p], plo = s.plo[p], prun = s.prun[p];
+        // (value, run) lookup of tail element c of pivot pp: the value may also
+        // sit in other rows' runs
+        auto probe = [&](uint32_t c, uint32_t slot, uint32_t run, uint32_t pp) {
+          const uint32_t tb = run >> 16, te = run & 0xffffu;
+          const uint32_t hh = a22_mix(c, te);
+          const uint32_t fb = a22_fbit(hh);
+          if (s.filt[fb >> 5] & (1u << (fb & 31))) {
+            uint32_t x = kChunk;
+            for (uint32_t h = a22_slot(hh);; h = (h + 1) & (kA22Table - 1)) {
+              const uint2 e = s.tab[h];
+              if (e.x == 0) break;
+              if (e.x == c && e.y - tb < te - tb) {
+                x = e.y;
+                break;
+              }
+            }
+            if (x < (uint32_t)kChunk) {
+              atomicAdd(&s.cntA[x], 1u);
+              atomicAdd(&S[slot], 1u);
+              if (pp != accP) {
+                if (accN) atomicAdd(&s.cntP[accP], accN);
+                accP = pp;
+                accN = 0;
+              }
+              ++accN;
+              ++tri_task;
             }
           }
-          if (x < (uint32_t)kChunk) {
-            atomicAdd(&s.cntA[x], 1u);
-            atomicAdd(&S[slot], 1u);
-            atomicAdd(&s.cntP[pp], 1u);
-            ++tri_task;
+        };
+        auto advance = [&](uint32_t f) {
+          if (f >= pe_) {
+            do {
+              ++p;
+              pe_ = s.pref[p + 1];
+            } while (pe_ <= f);
+            pb = s.pref[p];
+            plo = s.plo[p];
+            prun = s.prun[p];
           }
-        }
-      };
-      auto advance = [&](uint32_t f) {
-        if (f >= pe_) {
-          do {
-            ++p;
-            pe_ = s.pref[p + 1];
-          } while (pe_ <= f);
-          pb = s.pref[p];
-          plo = s.plo[p];
-          prun = s.prun[p];
-        }
-      };
-      // kA22Unroll elements per lane per step, every load issued before any probe
-      for (uint32_t f = base + lane; f < lim; f += 32 * kA22Unroll) {
-        uint32_t sl[kA22Unroll], ru[kA22Unroll], pv[kA22Unroll], cv[kA22Unroll];
+        };
+        // kA22Unroll elements per lane per step, every load issued before any probe
+        for (uint32_t f = base + lane; f < lim; f += 32 * kA22Unroll) {
+          uint32_t sl[kA22Unroll], ru[kA22Unroll], pv[kA22Unroll], cv[kA22Unroll];
 #pragma unroll
-        for (int u = 0; u < kA22Unroll; ++u) {
-          const uint32_t fu = f + 32 * u;
-          if (fu < lim) advance(fu);
-          sl[u] = plo + (fu - pb), ru[u] = prun, pv[u] = p;
+          for (int u = 0; u < kA22Unroll; ++u) {
+            const uint32_t fu = f + 32 * u;
+            if (fu < lim) advance(fu);
+            sl[u] = plo + (fu - pb), ru[u] = prun, pv[u] = p;
+          }
+#pragma unroll
+          for (int u = 0; u < kA22Unroll; ++u) cv[u] = (f + 32 * u < lim) ? col[sl[u]] : 0u;
+#pragma unroll
+          for (int u = 0; u < kA22Unroll; ++u)
+            if (f + 32 * u < lim) probe(cv[u], sl[u], ru[u], pv[u]);
         }
-#pragma unroll
-        for (int u = 0; u < kA22Unroll; ++u) cv[u] = (f + 32 * u < lim) ? col[sl[u]] : 0u;
-#pragma unroll
-        for (int u = 0; u < kA22Unroll; ++u)
-          if (f + 32 * u < lim) probe(cv[u], sl[u], ru[u], pv[u]);
+      }
+      if (accN) atomicAdd(&s.cntP[accP], accN);
+      tri_local += tri_task;
+      __syncthreads();
+
+      // 5a. flush this batch's pivot counts (the next batch reuses the slots)
+      {
+        const uint32_t cp = s.cntP[tid];
+        if (cp) atomicAdd(&S[s.ps[tid]], cp);
       }
     }
-    tri_local += tri_task;
-    __syncthreads();
 
-    // 5. flush shared counts (A22 slots, pivots)
+    if (COST && tid == 0) cost[t] = task_w;
+    // 5b. flush the staged chunk's A22 counts once per task
+    if (staged) {
 #pragma unroll
-    for (int e = 0; e < EPT; ++e) {
-      const uint32_t x = tid * EPT + e;
-      const uint32_t ca = s.cntA[x];
-      if (ca) atomicAdd(&S[a0 + x], ca);
-    }
-    {
-      const uint32_t cp = s.cntP[tid];
-      if (cp) atomicAdd(&S[s.ps[tid]], cp);
+      for (int e = 0; e < EPT; ++e) {
+        const uint32_t x = tid * EPT + e;
+        const uint32_t ca = s.cntA[x];
+        if (ca) atomicAdd(&S[a0 + x], ca);
+      }
     }
     __syncthreads();
   }
@@ -1090,7 +1130,8 @@ __global__ void k_chunk_first(const uint32_t* __restrict__ row_ptr, uint32_t n, 
   jfirst[q] = max(lo - 1, 1u);
 }
 
-// Load time: batches per chunk (pivots into the chunk's rows / kA22Batch).
+// Load time: tasks per chunk (batches of kA22Batch pivots into the chunk's
+// rows, kA22Group batches per task).
 __global__ void k_a22_count(const uint32_t* __restrict__ jfirst, const uint32_t* __restrict__ chunk_row,
                             const uint32_t* __restrict__ pin_off, uint32_t nchunks, uint32_t* __restrict__ cnt) {
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1100,14 +1141,38 @@ __global__ void k_a22_count(const uint32_t* __restrict__ jfirst, const uint32_t*
     return;
   }
   const uint32_t k0 = pin_off[jfirst[q]], k1 = pin_off[chunk_row[q] + 1];
-  cnt[q] = (k1 - k0 + kA22Batch - 1) / kA22Batch;
+  const uint32_t nb = (k1 - k0 + kA22Batch - 1) / kA22Batch;
+  cnt[q] = (nb + kA22Group - 1) / kA22Group;
 }
 
 __global__ void k_a22_fill(const uint32_t* __restrict__ cnt_off, uint32_t nchunks, uint2* __restrict__ tasks) {
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= nchunks) return;
   const uint32_t o = cnt_off[q], c = cnt_off[q + 1] - o;
-  for (uint32_t b = 0; b < c; ++b) tasks[o + b] = make_uint2(q, b);
+  for (uint32_t b = 0; b < c; ++b) tasks[o + b] = make_uint2(q, b * kA22Group);
+}
+
+// Multi-rank full pass: rank r takes the contiguous tasks
+// [lo, hi) whose exclusive work prefix pre[t] (over k_support_a22<true>'s
+// costs, pre[ntasks] = total) falls in [total*r/world, total*(r+1)/world);
+// every rank computes the same split from the same replicated state.
+__global__ void k_a22_split(DevState* st, const unsigned long long* __restrict__ pre, uint32_t ntasks,
+                            uint32_t rank, uint32_t world) {
+  if (st->mode) return;
+  const unsigned long long total = pre[ntasks];
+  auto first_at = [&](unsigned long long bound) {  // first t with pre[t] >= bound
+    uint32_t lo = 0, hi = ntasks;
+    while (lo < hi) {
+      const uint32_t mid = (lo + hi) >> 1;
+      if (pre[mid] < bound) lo = mid + 1; else hi = mid;
+    }
+    return lo;
+  };
+  const unsigned long long b0 = (unsigned long long)((__uint128_t)total * rank / world);
+  const unsigned long long b1 = (unsigned long long)((__uint128_t)total * (rank + 1) / world);
+  st->a22_lo = rank == 0 ? 0u : first_at(b0);
+  st->a22_hi = rank + 1 == world ? ntasks : first_at(b1);
+  st->task_next = 0;
 }
 
 // Paper Listing 1 / support.cpp:115-127 as written: one thread per slot,
@@ -1426,7 +1491,8 @@ k_mark(Graph g, Sym y) {
       if (sv < thr || u < h0) {
         rm = true;
         id = g.payload[p];
-        dcost += mark_removed<true>(g, y, (uint32_t)p, u, v, id);
+        const uint32_t c = mark_removed<true>(g, y, (uint32_t)p, u, v, id);
+        if (u < h0 || sv != 0) dcost += c;  // S = 0 (exact above h0): no triangle to carry
         if (!y.rdirty[u]) y.rdirty[u] = 1;
         if (!y.sdirty[u]) y.sdirty[u] = 1;
       } else {
@@ -1478,7 +1544,8 @@ k_mark_frontier(Graph g, Sym y) {
     const uint32_t id = fq[i];
     const uint32_t p = y.pos_of[id];
     const uint32_t u = y.erow[id];
-    dcost += mark_removed<false>(g, y, p, u, g.col[p], id);
+    const uint32_t c = mark_removed<false>(g, y, p, u, g.col[p], id);
+    if (cur_S(g)[p] != 0) dcost += c;  // carried S is exact: S = 0 closes no triangle
     y.rdirty[u] = 1;
     y.sdirty[u] = 1;
   }
@@ -1639,7 +1706,11 @@ k_delta(Graph g, Sym y) {
   const uint32_t par = g.st->fpar ^ 1u;  // next round's frontier
   uint32_t* __restrict__ fq_next = par ? y.fq1 : y.fq0;
   uint32_t* cnt_next = &g.st->nfq[par];
+  const uint32_t h0 = g.st->h0;
   auto edge = [&](uint32_t p, uint32_t u, uint32_t v) {
+    // S of a removed edge is its exact triangle count in G_r (rows below h0
+    // of a pristine round 0 excepted): S = 0 means no triangle loses an edge
+    if (u >= h0 && S[p] == 0) return;
     const uint32_t mn = min(y.deg[u], y.deg[v]);
     if (mn <= kDeltaInline) {
       delta_edge(g, y, S, fq_next, cnt_next, thr, p, u, v, 0, mn);

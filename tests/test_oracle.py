@@ -143,3 +143,55 @@ def test_planted_cliques_config(port):
     m = clique_members(1 << 10, 40, 43)
     assert len(set(m.tolist())) == 40
     assert port.kmax(g1, threads=4) == 40
+
+
+@pytest.mark.parametrize("scale,ef", [(10, 16), (13, 8), (12, 32)])
+def test_reference_side_generator_and_fast_canonicalize(ref, scale, ef):
+    """bench.py's reference arm builds its input on the reference side only:
+    the §8(d) generator restated in oracle/ref_capi.cpp, then either the
+    reference canonicalize or its parallel restatement -- byte-identical, and
+    identical to the product's generator (the large digests pin s20/s24)."""
+    import oracle
+    from paper_2009_07929_b200 import graph
+    extra = oracle.clique_pairs(1 << scale, (8, 20), 42) if ef == 32 else None
+    a = ref.rmat(scale, ef, 42, extra_pairs=extra, fast=True)
+    b = ref.rmat(scale, ef, 42, extra_pairs=extra, fast=False)
+    c = graph.rmat_cliques(scale, ef, 42, sizes=(8, 20)) if ef == 32 else graph.rmat(scale, ef, 42)
+    for x in (b, c):
+        assert np.array_equal(a.row_ptr, x.row_ptr) and np.array_equal(a.col_idx, x.col_idx)
+    e1 = ref.erdos_renyi(scale, ef << scale, 7, fast=True)
+    e2 = ref.erdos_renyi(scale, ef << scale, 7, fast=False)
+    assert np.array_equal(e1.col_idx, e2.col_idx) and np.array_equal(e1.row_ptr, e2.row_ptr)
+
+
+def test_reference_fine_sample_partitions_a_pass(ref):
+    """The cpu_baseline sample (support.cpp:115-127 over a chunk subset):
+    the stride phases together are exactly one compute_supports pass."""
+    g = ref.rmat(12, 16, 42)
+    _, tri, S = ref.compute_supports(g, 2, 2)
+    acc = np.zeros(g.total_slots(), np.uint32)
+    tot = 0
+    for ph in range(5):
+        t, acc, _ = ref.fine_sample(g, 5, ph, 2, acc)
+        tot += t
+    assert tot == tri and np.array_equal(acc, S)
+
+
+def test_large_golden_file_is_consistent():
+    """tests/golden/large_ref.json (reference digests at s20/s24/ER/cliques):
+    every fixpoint record ends in a zero-removal round, survivors fit the
+    graph, and s24's K_max claim is bracketed when both probes exist."""
+    import json
+    import os
+    p = os.path.join(os.path.dirname(__file__), "golden", "large_ref.json")
+    if not os.path.exists(p):
+        pytest.skip("large_ref.json not generated yet")
+    d = json.load(open(p))
+    for name, ent in d.items():
+        for k, fp in ent.get("fixpoints", {}).items():
+            assert fp["removed"][-1] == 0 and fp["iterations"] == len(fp["removed"])
+            assert 0 <= fp["survivors"] <= ent["m"]
+            assert ent["m"] - sum(fp["removed"]) == fp["survivors"], (name, k)
+    s24 = d.get("s24", {}).get("fixpoints", {})
+    if "935" in s24 and "936" in s24:
+        assert s24["935"]["survivors"] > 0 and s24["936"]["survivors"] == 0
