@@ -36,9 +36,11 @@ fixpoint takes minutes, so it runs 1 trial per K with no warm-up (BASELINE.md
 §3) and says so.
 
 Multi-GPU (torchrun, N>1): every fixpoint edge-partitioned over the ranks
-(engine_join: full support passes split by a work-balanced prefix sum of
-per-task cost, exact u32 ncclAllReduce of S, carried rounds' removal frontier
-sharded with an all-reduce of the decrements); total work fixed => "strong".
+(dist.engine_join_group: full support passes split by a prefix sum of the
+tasks' exact work, S all-reduced by kernels over NVLink peer memory; carried
+rounds' removals sharded by edge id, decrement lists exchanged the same way;
+one CUDA-graph launch per fixpoint per rank); total work fixed => "strong".
+--exchange nccl: the host-driven ncclAllReduce variant.
 --ks all: every K in 3..K_max (configs[1] style sweep), one at a time.
 """
 from __future__ import annotations
@@ -80,6 +82,9 @@ def parse():
     ap.add_argument("--e2e-steps", type=int, default=1)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-stride", type=int, default=64, help="cpu_baseline: 1/stride chunk sample of a pass")
+    ap.add_argument("--exchange", default="group", choices=["group", "nccl"],
+                    help="N>1: group = device-resident exchange over NVLink peer memory inside the fixpoint "
+                         "graph (sharded carried rounds); nccl = host-driven ncclAllReduce after full passes")
     ap.add_argument("--ref-budget-s", type=float, default=120.0,
                     help="reference arm: after one step longer than this, stop (1 trial, no warm-up)")
     return ap.parse_args()
@@ -346,8 +351,12 @@ def main():
     load_s = time.time() - t0
     kmax = KNOWN_KMAX.get(graph_key(args)) or eng.kmax()  # untimed (bench.cpp:25)
     ks = resolve_ks(args, kmax)
+    mapped = []
     if world > 1:
-        kd.engine_join(eng)
+        if args.exchange == "group":
+            mapped = kd.engine_join_group(eng)
+        else:
+            kd.engine_join(eng)
 
     # one synchronous pass: rounds / survivors per K (launch count, checks)
     rounds, live = {}, {}
@@ -493,8 +502,11 @@ def main():
             cpu = {"value": None, "unit": "edges/s", "cores": 0, "kind": "reference", "sample": f"unavailable: {ex}"}
 
     # k_set_live + k_begin + 13 per round + 2 triangle total + 4 publish, per
-    # fixpoint; multi-rank runs add one ncclAllReduce per full-pass round
-    launches = args.steps * sum(2 + 13 * rounds[k] + 2 + 4 for k in ks)
+    # fixpoint; a peer group adds 3 split + 3 all-reduce + 2 delta-exchange
+    # kernels per round (the ones a round does not need exit at once); the
+    # nccl exchange adds one ncclAllReduce (NCCL's kernel) per full pass
+    per_round = 13 + (8 if world > 1 and args.exchange == "group" else 0)
+    launches = args.steps * sum(2 + per_round * rounds[k] + 2 + 4 for k in ks)
     if rank == 0:
         cfg = base_config(args, ks, n, m, slots)
         cfg.update({
@@ -505,8 +517,13 @@ def main():
                   (slots * 4 / 1e6, ">" if slots * 4 > 126e6 else "<"),
             "prep_outside_timing": "working layout / symmetric rows / A22 plan built once at load "
                                    f"({load_s:.1f} s incl. H2D); e2e rebuilds it per K",
-            "parallelism": (f"edge-partitioned x{world} (full passes: A22 tasks split across ranks + "
-                            "ncclAllReduce of S; carried rounds replicated)")
+            "parallelism": ((f"edge-partitioned x{world}, device-resident group (full passes: A22 tasks "
+                             "split by a prefix sum of their exact work + in-kernel all-reduce of S over NVLink "
+                             "peer memory; carried rounds: removals sharded by edge id + decrement lists "
+                             "exchanged in-kernel; compaction replicated; one graph launch per fixpoint)")
+                            if args.exchange == "group" else
+                            (f"edge-partitioned x{world} (full passes: A22 tasks split by exact work + "
+                             "ncclAllReduce of S, host loop; carried rounds replicated)"))
                            if world > 1 else "single",
         })
         line = {
@@ -520,7 +537,10 @@ def main():
             "repo_libs_loaded": repo_libs(),
         }
         print(json.dumps(line), flush=True)
+    barrier()
     eng.close()
+    for p in mapped:
+        kt.truss.ipc_close(p)
     if world > 1:
         dist.destroy_process_group()
 

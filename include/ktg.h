@@ -248,11 +248,19 @@ ktg_status ktg_engine_device_state(ktg_engine* e, uint32_t** d_col_idx, uint32_t
 ktg_status ktg_engine_extract(ktg_engine* e, uint32_t* out_u, uint32_t* out_v,
                               uint32_t* out_support, uint64_t edge_cap, uint64_t* num_edges);
 
-/* Multi-GPU: this engine computes supports for its share of
- * the support tasks only (work-balanced split into `world` parts); the
- * caller all-reduces the support buffer between the support and prune steps
- * through the allreduce callback, invoked once per round on the engine stream
- * (host-driven loop). world == 1 restores single-GPU operation. */
+/* Multi-GPU, host-driven exchange: every full support pass
+ * covers this rank's share of the support tasks only -- in carried-support
+ * runs (the default) a contiguous range of the A22 tasks split by a prefix
+ * sum of their exact work on the current graph; in KTG_FLAG_RECOMPUTE runs a
+ * work-balanced range of chunk tasks -- and the caller all-reduces the
+ * support buffer through the allreduce callback on the engine stream. The
+ * callback runs after every FULL support pass only (carried rounds are
+ * replicated on every rank and need no exchange); it sums S only, and the
+ * engine derives the round's triangle count from the summed S in carried
+ * runs (in recompute runs with the callback, info.triangles is this rank's
+ * partial count). world == 1 restores single-GPU operation. Standalone
+ * support passes (ktg_engine_support_pass, compute_supports, the kmax bound)
+ * are never partitioned: every rank computes the whole pass. */
 typedef int (*ktg_allreduce_cb)(uint32_t* d_buf, uint64_t count, void* stream, void* user);
 ktg_status ktg_engine_set_partition(ktg_engine* e, uint32_t rank, uint32_t world,
                                     ktg_allreduce_cb allreduce, void* user);
@@ -296,6 +304,33 @@ ktg_status ktg_device_copy(void* dst, const void* src, uint64_t bytes, void* str
 ktg_status ktg_ipc_handle(const void* d_ptr, uint8_t* out_64_bytes);
 ktg_status ktg_ipc_open(const uint8_t* handle_64_bytes, void** d_ptr);
 ktg_status ktg_ipc_close(void* d_ptr);
+
+/* Peer group (the device-resident partitioned fixpoint): the
+ * exchange runs as kernels over NVLink peer memory inside the fixpoint's
+ * CUDA graph, so a partitioned fixpoint is ONE graph launch with no host
+ * round trip per round:
+ *   full pass   this rank's work-balanced range of the A22 tasks, then a
+ *               device barrier, a reduce of this rank's span of S over every
+ *               rank's partial buffer written back to every rank (reduce-
+ *               scatter + all-gather in one kernel), and a second barrier;
+ *   carried     the round's removed edges are sharded by a hash of the edge
+ *   round       id; each rank finds the lost triangles of its share, applies
+ *               the decrements locally and lists them in its exchange area;
+ *               after a device barrier every rank applies its peers' lists.
+ *               Compaction stays replicated (deterministic, same on every rank).
+ * Setup (after ktg_engine_load, collective): every rank allocates its area
+ * with ktg_engine_group_area, shares it and its support buffers
+ * (ktg_engine_support_buffers) with the peers (ktg_ipc_handle / ktg_ipc_open
+ * across processes, plain pointers within one), then calls
+ * ktg_engine_set_group with the tables of every rank's area / S0 / S1 mapped
+ * into this process (own entry at `rank`), then all ranks meet in a host
+ * barrier before the first run. Every rank must run the same sequence of
+ * fixpoints (same k). A rank that stops joining barriers makes its peers fail
+ * with KTG_ERR_CUDA ("peer group barrier timed out") after 120 s. Loading
+ * another graph leaves the group (set it up again). */
+ktg_status ktg_engine_group_area(ktg_engine* e, void** d_area, uint64_t* bytes);
+ktg_status ktg_engine_set_group(ktg_engine* e, uint32_t rank, uint32_t world, void* const* areas,
+                                uint32_t* const* peer_s0, uint32_t* const* peer_s1);
 
 #ifdef __cplusplus
 }

@@ -217,6 +217,12 @@ struct ktg_engine {
   ktg_peer_cb peer_cb = nullptr;
   void* peer_user = nullptr;
   ncclComm_t nccl = nullptr;
+  // peer group (ktg_engine_set_group): own exchange area, device tables of
+  // every rank's area and support buffers, list capacity, reduce span
+  bool group = false;
+  DBuf<unsigned char> xarea;
+  DBuf<void*> xtab;
+  uint64_t xcap = 0, xspan = 0;
 
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evs0 = nullptr, evs1 = nullptr;
   ktg_run_info info{};
@@ -248,6 +254,8 @@ struct ktg_engine {
     g.peer1 = npeer ? peer_tab.p + npeer : nullptr;
     g.span = peer_span;
     g.npeer = npeer;
+    g.xa = (group && world > 1) ? reinterpret_cast<XArea*>(xarea.p) : nullptr;
+    g.xcap = xcap;
     return g;
   }
 
@@ -271,6 +279,19 @@ struct ktg_engine {
     return y;
   }
 
+  XGroup xgroup() {
+    XGroup x;
+    void** t = xtab.p;
+    x.area = reinterpret_cast<XArea* const*>(t);
+    x.S0 = reinterpret_cast<uint32_t* const*>(t + world);
+    x.S1 = reinterpret_cast<uint32_t* const*>(t + 2 * (size_t)world);
+    x.rank = rank_id;
+    x.world = world;
+    x.cap = xcap;
+    x.span = xspan;
+    return x;
+  }
+
   void free_all() {
     if (exec) cudaGraphExecDestroy(exec);
     exec = nullptr;
@@ -292,6 +313,9 @@ struct ktg_engine {
     task_cost.release();
     task_pre.release();
     peer_tab.release();
+    xarea.release();
+    xtab.release();
+    group = false;
     dead.release();
     rdirty.release();
     sdirty.release();
@@ -671,6 +695,17 @@ ktg_status engine_load(ktg_engine* e, const uint32_t* row_ptr, uint32_t n, const
   Layout& C = e->cl;
   C.ready = false;
   e->wl.ready = false;
+  // a peer group survives a reload only if the peers' tables still describe
+  // this engine's buffers (same allocations, same slot count, lists large
+  // enough) -- every rank reloading the same graph, as a multi-GPU e2e does
+  const bool had_group = e->group;
+  const uint32_t g_rank = e->rank_id, g_world = e->world;
+  const void* g_bufs[3] = {e->act().S0.p, e->act().S1.p, (void*)e->act().slots};
+  if (had_group) {
+    e->group = false;
+    e->world = 1;
+    e->rank_id = 0;
+  }
   if (row_ptr || col) e->has_orig_ids = false;
   C.n = n;
   C.slots = slots;
@@ -694,6 +729,12 @@ ktg_status engine_load(ktg_engine* e, const uint32_t* row_ptr, uint32_t n, const
     mark("working layout (+ symmetric rows)");
     if (with_sym) KTG_TRY(build_sym(e));
     mark("A22 plan");
+  }
+  if (had_group && e->act().S0.p == g_bufs[0] && e->act().S1.p == g_bufs[1] &&
+      (void*)e->act().slots == g_bufs[2] && e->xcap >= e->act().live_pristine) {
+    e->group = true;
+    e->world = g_world;
+    e->rank_id = g_rank;
   }
   return KTG_OK;
 }
@@ -886,8 +927,23 @@ ktg_status enqueue_round(ktg_engine* e, bool graph_mode, cudaGraphConditionalHan
     k_support_chunked<<<e->support_grid, kSupportThreads, e->support_smem, s>>>(g);
   }
   if (sup1) KTG_CUDA(cudaEventRecord(sup1, s));
+  const bool grp = e->group && e->world > 1;
+  if (grp) {
+    // device-side all-reduce of the partial supports over peer memory: carried
+    // runs after full passes only, recompute runs every round
+    const XGroup x = e->xgroup();
+    if (e->inc_active) {
+      k_xbar<0><<<1, 32, 0, s>>>(e->d_st, x, 1);
+      k_xreduce<<<4 * e->num_sms, 256, 0, s>>>(g, x, 1);
+      k_xbar<0><<<1, 32, 0, s>>>(e->d_st, x, 0);
+    } else {
+      k_xbar<2><<<1, 32, 0, s>>>(e->d_st, x, 1);
+      k_xreduce<<<4 * e->num_sms, 256, 0, s>>>(g, x, 0);
+      k_xbar<2><<<1, 32, 0, s>>>(e->d_st, x, 0);
+    }
+  }
   if (e->inc_active) {
-    if (!graph_mode && e->world > 1 && e->h_st->mode == 0 && (e->nccl || e->allreduce)) {
+    if (!grp && !graph_mode && e->world > 1 && e->h_st->mode == 0 && (e->nccl || e->allreduce)) {
       // multi-rank carried run: this full pass covered this rank's A22
       // tasks only; sum the partial supports, then every rank runs the same
       // deterministic mark / delta / compaction on identical data
@@ -905,10 +961,15 @@ ktg_status enqueue_round(ktg_engine* e, bool graph_mode, cudaGraphConditionalHan
     const Sym y = e->sym();
     k_mark<<<e->prune_grid, kPruneThreads, 0, s>>>(g, y);
     k_mark_frontier<<<e->prune_grid, kPruneThreads, 0, s>>>(g, y);
-    k_decide<<<1, 1, 0, s>>>(e->d_st);
+    k_decide<<<1, 1, 0, s>>>(e->d_st, grp ? reinterpret_cast<XArea*>(e->xarea.p) : nullptr, e->xcap);
     k_queues<<<4 * e->num_sms, 256, 0, s>>>(g, y);
     k_delta<<<e->prune_grid, kPruneThreads, 0, s>>>(g, y);
     k_delta_big<<<e->prune_grid, kPruneThreads, 0, s>>>(g, y);
+    if (grp) {  // every rank's listed decrements reach every rank
+      const XGroup x = e->xgroup();
+      k_xbar<1><<<1, 32, 0, s>>>(e->d_st, x, 0);
+      k_xapply<<<e->prune_grid, kPruneThreads, 0, s>>>(g, y, x);
+    }
     k_inc_rows<0><<<e->prune_grid, kPruneThreads, 0, s>>>(g, y);
     k_inc_rows<1><<<e->heavy_grid, kSymHeavyThreads, 0, s>>>(g, y);
     k_inc_sym<0><<<e->prune_grid, kPruneThreads, 0, s>>>(g, y);
@@ -920,7 +981,9 @@ ktg_status enqueue_round(ktg_engine* e, bool graph_mode, cudaGraphConditionalHan
   }
   if (e->opt.width_bits == 16) k_check16<<<4 * e->num_sms, 256, 0, s>>>(g);
   KTG_CUDA(cudaGetLastError());
-  if (!graph_mode && e->npeer > 1 && e->peer_cb) {
+  if (grp) {
+    // exchanged above
+  } else if (!graph_mode && e->npeer > 1 && e->peer_cb) {
     // fused path: the support kernel already sent every increment to its
     // owner; the callback waits for all ranks, all-gathers the owned spans
     // and sums the round's triangle count
@@ -950,7 +1013,9 @@ ktg_status enqueue_round(ktg_engine* e, bool graph_mode, cudaGraphConditionalHan
 ktg_status build_graph(ktg_engine* e) {
   Layout& L = e->act();
   const void* key[4] = {L.col.p, L.id.p, L.S0.p, L.pairs.p};
-  const uint64_t key2[4] = {L.slots, L.n, (uint64_t)(flag(e, KTG_FLAG_NAIVE_SUPPORT) ? 1 : 0),
+  const uint64_t key2[4] = {L.slots, L.n,
+                            (uint64_t)(flag(e, KTG_FLAG_NAIVE_SUPPORT) ? 1 : 0) | ((uint64_t)e->group << 1) |
+                                ((uint64_t)e->world << 8) | ((uint64_t)e->rank_id << 32),
                             (uint64_t)e->opt.width_bits | ((uint64_t)e->reoriented << 8) |
                                 ((uint64_t)e->scan_ratio << 16) | ((uint64_t)e->inc_active << 48)};
   if (e->exec && std::equal(key, key + 4, e->exec_key) && std::equal(key2, key2 + 4, e->exec_key2))
@@ -1000,7 +1065,7 @@ ktg_status build_graph(ktg_engine* e) {
 bool inc_eligible(const ktg_engine* e) {
   return e->reoriented && e->sym_ready && !flag(e, KTG_FLAG_RECOMPUTE) && !flag(e, KTG_FLAG_NAIVE_SUPPORT) &&
          e->opt.width_bits == 32 && e->opt.observer == nullptr && e->npeer <= 1 &&
-         (e->world == 1 || e->nccl != nullptr || e->allreduce != nullptr);
+         (e->world == 1 || e->nccl != nullptr || e->allreduce != nullptr || e->group);
 }
 
 ktg_status begin_run(ktg_engine* e, uint32_t k, int parity) {
@@ -1059,7 +1124,7 @@ ktg_status run_loop(ktg_engine* e, bool want_sync) {
   const bool timing = flag(e, KTG_FLAG_TIME_SUPPORT);
   const bool recording = timing || flag(e, KTG_FLAG_COLLECT_WORK);
   const bool host_loop =
-      flag(e, KTG_FLAG_HOST_LOOP) || e->opt.observer || (e->world > 1) || e->nccl || recording;
+      flag(e, KTG_FLAG_HOST_LOOP) || e->opt.observer || (e->world > 1 && !e->group) || e->nccl || recording;
   e->work.clear();
   e->caller_stale = true;
   KTG_CUDA(cudaEventRecord(e->ev0, e->stream));
@@ -1119,6 +1184,8 @@ ktg_status run_loop(ktg_engine* e, bool want_sync) {
 }
 
 ktg_status overflow_error(ktg_engine* e) {
+  if (e->h_st->error == kErrGroupTimeout)
+    return fail(KTG_ERR_CUDA, "peer group barrier timed out (a rank stopped joining the fixpoint)");
   const unsigned long long key = e->h_st->overflow_slot;
   const uint64_t slot = key >> 32;
   const uint32_t cnt = (uint32_t)(key & 0xffffffffull);
@@ -1162,7 +1229,7 @@ ktg_status support_pass(ktg_engine* e, int parity, uint64_t* triangles, bool max
     uint32_t rank, world, npeer;
     ~Solo() { e->rank_id = rank, e->world = world, e->npeer = npeer; }
   } solo{e, e->rank_id, e->world, e->npeer};
-  e->rank_id = 0, e->world = 1, e->npeer = 0;
+  e->rank_id = 0, e->world = 1, e->npeer = 0;  // (graph_of: no group area at world 1)
   Graph g = e->graph_of(L);
   e->inc_active = false;
   k_begin<<<1, 1, 0, e->stream>>>(e->d_st, 0, e->opt.width_bits == 16 ? 1 : 0, parity, 0u, e->delta_ratio, e->delta_ratio0);
@@ -1554,6 +1621,7 @@ static void drop_exchanges(ktg_engine* e, bool nccl, bool peers, bool cb) {
     e->npeer = 0;
     e->peer_cb = nullptr;
     e->peer_user = nullptr;
+    e->group = false;
   }
   if (cb) {
     e->allreduce = nullptr;
@@ -1622,6 +1690,69 @@ ktg_status ktg_engine_set_peers(ktg_engine* e, uint32_t rank, uint32_t world, ui
   }
   if (e->exec) cudaGraphExecDestroy(e->exec);
   e->exec = nullptr;
+  return KTG_OK;
+}
+
+__global__ void k_set_xepoch(DevState* st, unsigned int v) { st->xepoch = v; }
+
+ktg_status ktg_engine_group_area(ktg_engine* e, void** d_area, uint64_t* bytes) {
+  Layout& L = e->act();
+  if (!L.ready) return fail(KTG_ERR_INVALID_PARAMETER, "load the graph before ktg_engine_group_area");
+  // one list entry per pristine live edge: a carrying round lists at most
+  // 2 * delta_cost decrements and k_decide recomputes instead when that
+  // could exceed it
+  const uint64_t cap = std::max<uint64_t>(L.live_pristine, 1024);
+  const size_t need = sizeof(XArea) + 2 * cap * sizeof(uint32_t);
+  KTG_TRY(e->xarea.ensure(need));
+  KTG_CUDA(cudaMemsetAsync(e->xarea.p, 0, sizeof(XArea), e->stream));
+  KTG_CUDA(cudaStreamSynchronize(e->stream));
+  e->xcap = cap;
+  if (d_area) *d_area = e->xarea.p;
+  if (bytes) *bytes = need;
+  return KTG_OK;
+}
+
+ktg_status ktg_engine_set_group(ktg_engine* e, uint32_t rank, uint32_t world, void* const* areas,
+                                uint32_t* const* peer_s0, uint32_t* const* peer_s1) {
+  if (world == 0 || rank >= world) return fail(KTG_ERR_INVALID_PARAMETER, "rank must be < world");
+  if (world > (uint32_t)kMaxGroup) return fail(KTG_ERR_INVALID_PARAMETER, "peer group larger than 64 ranks");
+  Layout& L = e->act();
+  if (!L.ready) return fail(KTG_ERR_INVALID_PARAMETER, "load the graph before ktg_engine_set_group");
+  drop_exchanges(e, true, true, true);
+  e->rank_id = 0;
+  e->world = 1;
+  if (e->exec) cudaGraphExecDestroy(e->exec);
+  e->exec = nullptr;
+  if (world == 1) return KTG_OK;
+  if (!areas || !peer_s0 || !peer_s1) return fail(KTG_ERR_INVALID_PARAMETER, "world > 1 needs the peer tables");
+  if (!e->xarea.p || e->xcap == 0 || areas[rank] != e->xarea.p)
+    return fail(KTG_ERR_INVALID_PARAMETER, "area table must hold this engine's ktg_engine_group_area at its rank");
+  if (peer_s0[rank] != L.S0.p || peer_s1[rank] != L.S1.p)
+    return fail(KTG_ERR_INVALID_PARAMETER, "peer tables must hold this engine's own support buffers at its rank");
+  std::vector<void*> tab(3 * (size_t)world);
+  for (uint32_t r = 0; r < world; ++r) {
+    tab[r] = areas[r];
+    tab[world + r] = peer_s0[r];
+    tab[2 * (size_t)world + r] = peer_s1[r];
+  }
+  KTG_TRY(e->xtab.ensure(tab.size()));
+  KTG_CUDA(cudaMemcpy(e->xtab.p, tab.data(), tab.size() * sizeof(void*), cudaMemcpyHostToDevice));
+  KTG_CUDA(cudaMemsetAsync(e->xarea.p, 0, sizeof(XArea), e->stream));
+  k_set_xepoch<<<1, 1, 0, e->stream>>>(e->d_st, 0u);
+  KTG_CUDA(cudaGetLastError());
+  e->xspan = ((L.slots + world - 1) / world + 3) / 4 * 4;
+  e->rank_id = rank;
+  e->world = world;
+  e->group = true;
+  // recompute runs plan a work-balanced chunk split every round inside the
+  // captured graph: size its buffers now
+  const size_t nq = (size_t)L.nchunks + 1;
+  KTG_TRY(e->task_cost.ensure(nq));
+  KTG_TRY(e->task_pre.ensure(nq));
+  size_t tmp = 0;
+  KTG_CUDA(cub::DeviceScan::ExclusiveSum(nullptr, tmp, e->task_cost.p, e->task_pre.p, (int)nq, e->stream));
+  KTG_TRY(e->cub_tmp.ensure(tmp));
+  KTG_CUDA(cudaStreamSynchronize(e->stream));
   return KTG_OK;
 }
 

@@ -74,7 +74,27 @@ struct DevState {
   unsigned int dq_lo, dq_hi;         // this rank's diagonal support tasks: chunks [dq_lo, dq_hi)
   unsigned long long rq_cap;         // delta piece queue capacity (a round that could exceed it recomputes)
   unsigned int a22_lo, a22_hi;       // this rank's A22 tasks [lo, hi) of the current full pass (world > 1)
+  unsigned int xepoch;               // peer group: barriers passed (never reset by a run)
+  unsigned int pad4;
 };
+
+constexpr unsigned int kErrGroupTimeout = 2;  // DevState::error: a peer never reached a barrier
+
+// Peer group (multi-GPU, ktg_engine_set_group): the exchange area each rank
+// keeps in its own HBM and every rank maps (CUDA IPC / peer access).
+constexpr int kMaxGroup = 64;
+struct XArea {
+  unsigned int flags[kMaxGroup];  // barrier: the epoch rank q has reached (written by q)
+  unsigned long long tri;         // this rank's partial triangle count of the current full pass
+  unsigned int cnt[2];            // lengths of this rank's decrement lists (round parity)
+  unsigned int pad[28];
+  // followed by 2 lists of `cap` edge ids: the surviving edges this rank's
+  // share of a carried round decremented
+};
+static_assert(sizeof(XArea) % 16 == 0, "lists start 16-byte aligned");
+__host__ __device__ __forceinline__ uint32_t* xlist(XArea* a, uint64_t cap, uint32_t par) {
+  return reinterpret_cast<uint32_t*>(a + 1) + par * cap;
+}
 
 struct Graph {
   const uint32_t* row_ptr;  // n+2
@@ -102,7 +122,18 @@ struct Graph {
   uint32_t* const* peer1;   // per rank: its S1
   uint64_t span;            // slots owned per rank
   uint32_t npeer;
+  // peer group: this rank's exchange area (null: no group); a carried
+  // round's removals are sharded by owner_of(edge id) and every decrement is
+  // also listed for the peers (k_xapply)
+  XArea* xa;
+  uint64_t xcap;
 };
+
+// Rank owning removed edge id in a sharded carried round (a hash, so the
+// split does not follow the caller's row order).
+__host__ __device__ __forceinline__ uint32_t owner_of(uint32_t id, uint32_t world) {
+  return (uint32_t)(((uint64_t)(id * 2654435761u) * world) >> 32);
+}
 
 // One support increment: local buffer, or the owning rank's buffer when the
 // support pass is fused with the reduce-scatter.
@@ -949,9 +980,14 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ cost) {
           }
           if (thi > tlo) {
             cost = thi - tlo;
-            s.ps[tid] = ps;
+            // pristine round 0 with the degree bound: rows below h0 go in
+            // this round whatever their counts (k_mark), so their slots --
+            // the pivot (i, j) and its tail (i, c) -- need no increments;
+            // bit 31 of the run marks such a pivot
+            const bool light = i < h0;
+            s.ps[tid] = light ? 0xffffffffu : ps;
             s.plo[tid] = tlo;
-            s.prun[tid] = run;
+            s.prun[tid] = run | (light ? 0x80000000u : 0u);
           }
         }
       }
@@ -1035,7 +1071,7 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ cost) {
         // (value, run) lookup of tail element c of pivot pp: the value may also
         // sit in other rows' runs
         auto probe = [&](uint32_t c, uint32_t slot, uint32_t run, uint32_t pp) {
-          const uint32_t tb = run >> 16, te = run & 0xffffu;
+          const uint32_t tb = (run >> 16) & 0x7fffu, te = run & 0xffffu;
           const uint32_t hh = a22_mix(c, te);
           const uint32_t fb = a22_fbit(hh);
           if (s.filt[fb >> 5] & (1u << (fb & 31))) {
@@ -1050,13 +1086,15 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ cost) {
             }
             if (x < (uint32_t)kChunk) {
               atomicAdd(&s.cntA[x], 1u);
-              atomicAdd(&S[slot], 1u);
-              if (pp != accP) {
-                if (accN) atomicAdd(&s.cntP[accP], accN);
-                accP = pp;
-                accN = 0;
+              if (!(run >> 31)) {
+                atomicAdd(&S[slot], 1u);
+                if (pp != accP) {
+                  if (accN) atomicAdd(&s.cntP[accP], accN);
+                  accP = pp;
+                  accN = 0;
+                }
+                ++accN;
               }
-              ++accN;
               ++tri_task;
             }
           }
@@ -1095,7 +1133,7 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ cost) {
       // 5a. flush this batch's pivot counts (the next batch reuses the slots)
       {
         const uint32_t cp = s.cntP[tid];
-        if (cp) atomicAdd(&S[s.ps[tid]], cp);
+        if (cp) atomicAdd(&S[s.ps[tid]], cp);  // light pivots never count (cp = 0)
       }
     }
 
@@ -1607,14 +1645,17 @@ __global__ void k_heavy_rank(DevState* st, const uint32_t* __restrict__ symdeg_p
 __global__ void k_set_pristine(DevState* st) { st->pristine = 1; }
 
 // One thread: this round's removal count is final; choose carry vs recompute.
-__global__ void k_decide(DevState* st) {
+__global__ void k_decide(DevState* st, XArea* xa, unsigned long long xcap) {
   if (st->mode == 1) st->keep_cost = st->live_cost > st->delta_cost ? st->live_cost - st->delta_cost : 0;
-  // pieces queued <= delta_cost / kDeltaPiece + removed: carry only if they fit
+  // pieces queued <= delta_cost / kDeltaPiece + removed: carry only if they
+  // fit; peer group: the decrements (<= 2 per lost triangle <= 2 delta_cost)
+  // must fit this round's list
   st->carry = (st->inc && st->removed != 0 &&
                (double)st->delta_cost <= (st->pristine ? st->delta_ratio0 : st->delta_ratio) * (double)st->keep_cost &&
-               st->delta_cost / kDeltaPiece + st->removed <= st->rq_cap)
+               st->delta_cost / kDeltaPiece + st->removed <= st->rq_cap && (!xa || 2 * st->delta_cost <= xcap))
                   ? 1u
                   : 0u;
+  if (xa) xa->cnt[st->iter & 1u] = 0;  // peers read the other parity's list (k_xapply)
 }
 
 __device__ __forceinline__ uint32_t lb_run(const uint32_t* __restrict__ a, uint32_t n, uint32_t key) {
@@ -1635,6 +1676,10 @@ __device__ __forceinline__ void drop_support(const Graph& g, const Sym& y, uint3
                                              uint32_t id) {
   const uint32_t old = atomicSub(&S[y.pos_of[id]], 1u);
   if (old == thr) append_coalesced(cnt_next, fq_next, id);
+  if (g.xa) {  // peer group: the peers apply the same decrement (k_xapply)
+    const uint32_t par = g.st->iter & 1u;
+    append_coalesced(&g.xa->cnt[par], xlist(g.xa, g.xcap, par), id);
+  }
 }
 
 // Triangles of G_r through the removed edge e = (u, v) at working slot p:
@@ -1711,6 +1756,7 @@ k_delta(Graph g, Sym y) {
     // S of a removed edge is its exact triangle count in G_r (rows below h0
     // of a pristine round 0 excepted): S = 0 means no triangle loses an edge
     if (u >= h0 && S[p] == 0) return;
+    if (g.xa && owner_of(g.payload[p], g.world) != g.rank) return;  // a peer's share
     const uint32_t mn = min(y.deg[u], y.deg[v]);
     if (mn <= kDeltaInline) {
       delta_edge(g, y, S, fq_next, cnt_next, thr, p, u, v, 0, mn);
@@ -1747,6 +1793,126 @@ k_delta_big(Graph g, Sym y) {
   for (uint32_t t = warp; t < ntask; t += nwarps) {
     const uint4 q = y.rq[t];
     delta_edge(g, y, S, fq_next, cnt_next, thr, q.x, q.y, q.z, q.w * kDeltaPiece, (q.w + 1) * kDeltaPiece);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Peer group exchange (multi-GPU, ktg_engine_set_group): collectives as
+// kernels over NVLink peer memory, so a partitioned fixpoint stays one
+// CUDA-graph launch with no host round trip per round.
+//   full pass: [this rank's A22 tasks] -> k_xbar -> k_xreduce (rank r sums
+//              every rank's partial S over its span and writes the sum back
+//              to every rank) -> k_xbar
+//   carried round: k_delta on this rank's removals -> k_xbar -> k_xapply
+//              (every peer's listed decrements applied locally)
+// Every rank runs the same control flow on replicated state, so all ranks
+// meet the same barriers in the same order.
+// ---------------------------------------------------------------------------
+struct XGroup {
+  XArea* const* area;      // per rank, peer-mapped (own at [rank])
+  uint32_t* const* S0;     // per rank: its support buffers (peer-mapped)
+  uint32_t* const* S1;
+  uint32_t rank, world;
+  uint64_t cap;            // entries per decrement list
+  uint64_t span;           // slots reduced per rank (multiple of 4)
+};
+
+__device__ __forceinline__ unsigned int ld_acquire_sys(const unsigned int* p) {
+  unsigned int v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(unsigned int* p, unsigned int v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned long long globaltimer_ns() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+// WHEN 0: after a carried run's full pass (mode 0); 1: in a carrying round;
+// 2: every round (recompute runs). One thread: publish (optionally) the
+// round's partial triangle count, signal every rank, wait for every rank.
+// A peer that never arrives (crashed rank) stops the loop after 120 s with
+// kErrGroupTimeout instead of hanging the device.
+template <int WHEN>
+__global__ void k_xbar(DevState* st, XGroup x, int publish_tri) {
+  if (WHEN == 0 && (st->mode != 0 || !st->inc)) return;
+  if (WHEN == 1 && !st->carry) return;
+  if (threadIdx.x != 0 || st->error) return;
+  XArea* own = x.area[x.rank];
+  if (publish_tri) *reinterpret_cast<volatile unsigned long long*>(&own->tri) = st->triangles;
+  const unsigned int ep = ++st->xepoch;
+  __threadfence_system();
+  for (uint32_t q = 0; q < x.world; ++q) st_release_sys(&x.area[q]->flags[x.rank], ep);
+  const unsigned long long t0 = globaltimer_ns();
+  for (uint32_t q = 0; q < x.world; ++q) {
+    while ((int)(ld_acquire_sys(&own->flags[q]) - ep) < 0) {
+      __nanosleep(128);
+      if (globaltimer_ns() - t0 > 120000000000ull) {
+        st->error = kErrGroupTimeout;
+        return;
+      }
+    }
+  }
+  __threadfence_system();
+}
+
+// Rank r's span of the support buffer: sum of every rank's partial counts,
+// written back to every rank (reduce-scatter + all-gather in one pass over
+// peer memory); block 0 also totals the round's triangle count.
+__global__ void k_xreduce(Graph g, XGroup x, int inc) {
+  if (inc && g.st->mode != 0) return;
+  if (g.st->error) return;
+  uint32_t* const* tab = g.st->parity ? x.S1 : x.S0;
+  const uint64_t lo = (uint64_t)x.rank * x.span;
+  const uint64_t hi = umin64(g.slots, lo + x.span);
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    unsigned long long t = 0;
+    for (uint32_t q = 0; q < x.world; ++q) t += *reinterpret_cast<volatile unsigned long long*>(&x.area[q]->tri);
+    g.st->triangles = t;
+  }
+  if (lo >= hi) return;
+  const uint64_t n4 = (hi - lo) / 4;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n4; i += stride) {
+    uint4 acc = make_uint4(0, 0, 0, 0);
+    for (uint32_t q = 0; q < x.world; ++q) {
+      const uint4 v = __ldcv(reinterpret_cast<const uint4*>(tab[q] + lo) + i);
+      acc.x += v.x, acc.y += v.y, acc.z += v.z, acc.w += v.w;
+    }
+    for (uint32_t q = 0; q < x.world; ++q) __stcg(reinterpret_cast<uint4*>(tab[q] + lo) + i, acc);
+  }
+  for (uint64_t i = lo + 4 * n4 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < hi; i += stride) {
+    uint32_t acc = 0;
+    for (uint32_t q = 0; q < x.world; ++q) acc += __ldcv(tab[q] + i);
+    for (uint32_t q = 0; q < x.world; ++q) __stcg(tab[q] + i, acc);
+  }
+}
+
+// Carrying round, after k_xbar<1>: every peer's decrements of this round
+// applied to the local supports (frontier crossings queued as in k_delta).
+__global__ void __launch_bounds__(kPruneThreads)
+k_xapply(Graph g, Sym y, XGroup x) {
+  if (!g.st->carry || g.st->error) return;
+  uint32_t* __restrict__ S = cur_S(g);
+  const uint32_t thr = g.st->threshold;
+  const uint32_t par = g.st->fpar ^ 1u;
+  uint32_t* __restrict__ fq_next = par ? y.fq1 : y.fq0;
+  uint32_t* cnt_next = &g.st->nfq[par];
+  const uint32_t lp = g.st->iter & 1u;
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint32_t q = 0; q < x.world; ++q) {
+    if (q == x.rank) continue;
+    XArea* a = x.area[q];
+    const uint32_t n = *reinterpret_cast<volatile unsigned int*>(&a->cnt[lp]);
+    const uint32_t* list = xlist(a, x.cap, lp);
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += stride) {
+      const uint32_t id = __ldcv(list + i);
+      const uint32_t old = atomicSub(&S[y.pos_of[id]], 1u);
+      if (old == thr) append_coalesced(cnt_next, fq_next, id);
+    }
   }
 }
 

@@ -1,18 +1,24 @@
 """Multi-GPU plumbing: one process per GPU, torch.distributed
 for rendezvous; the data path is the engine's own ncclAllReduce.
 
-Two ways the path shards:
+Three ways the path shards:
   * K sweep   -- K values are independent fixpoints on a replicated graph:
                  split_k_values() hands each rank a share, no collective;
   * one big fixpoint -- every full support pass covers this rank's share
-                 of the tasks (A22 tasks round-robin in carried runs, work-
+                 of the tasks (A22 tasks split by their exact work in carried runs, work-
                  balanced chunk ranges in recompute runs); the partial
                  supports are all-reduced (engine_join(): ncclAllReduce,
                  exact u32 sums) or, fused (engine_join_fused(), recompute
                  runs), every increment goes straight to the owner rank's
                  buffer over NVLink peer memory during the support pass and
                  only the owned spans are all-gathered; then every rank runs
-                 the same deterministic prune / carried rounds.
+                 the same deterministic prune / carried rounds;
+  * device-resident group (engine_join_group(), the default for bench.py
+                 --gpus N) -- the same split of full passes with the
+                 all-reduce done by kernels over NVLink peer memory inside
+                 the fixpoint's CUDA graph, and the carried rounds' removals
+                 sharded across ranks with their decrements exchanged the
+                 same way: one graph launch per fixpoint, no host round trip.
 """
 from __future__ import annotations
 
@@ -59,6 +65,39 @@ def engine_join(engine: Engine, group: Optional[dist.ProcessGroup] = None) -> No
     (collective)."""
     world, rank = world_rank()
     engine.set_nccl(rank, world, broadcast_nccl_id(group))
+
+
+def engine_join_group(engine: Engine, group: Optional[dist.ProcessGroup] = None) -> list:
+    """Device-resident partitioned fixpoint (ktg_engine_set_group): shares
+    this rank's exchange area and support buffers as CUDA IPC handles over
+    torch.distributed (collective), maps every peer's, installs the group and
+    meets the peers in a barrier. Every fixpoint then runs as one CUDA-graph
+    launch per rank: full passes split by work, S all-reduced by kernels over
+    NVLink peer memory; carried rounds' removals sharded, decrements
+    exchanged the same way. Call after engine.load(); returns the mapped peer
+    pointers (ipc_close them once the engine is done)."""
+    world, rank = world_rank()
+    area, _ = engine.group_area()
+    s0, s1, _ = engine.support_buffers()
+    mine = (ipc_handle(area), ipc_handle(s0), ipc_handle(s1))
+    allh = [None] * world
+    dist.all_gather_object(allh, mine, group=group)
+    mapped = []
+
+    def table(i, own):
+        out = []
+        for q in range(world):
+            if q == rank:
+                out.append(own)
+            else:
+                p = ipc_open(allh[q][i])
+                mapped.append(p)
+                out.append(p)
+        return out
+
+    engine.set_group(rank, world, table(0, area), table(1, s0), table(2, s1))
+    dist.barrier(group=group)
+    return mapped
 
 
 def max_over_ranks(x: float, device: Optional[torch.device] = None) -> float:

@@ -217,6 +217,11 @@ def lib():
         L.ktg_ipc_close.argtypes = [_vp]
         L.ktg_nccl_unique_id.argtypes = [_vp]
         L.ktg_engine_set_nccl.argtypes = [_vp, _u32, _u32, _vp]
+        try:  # (older builds used for A/B timing lack the peer group)
+            L.ktg_engine_group_area.argtypes = [_vp, P(_vp), P(_u64)]
+            L.ktg_engine_set_group.argtypes = [_vp, _u32, _u32, _vp, _vp, _vp]
+        except AttributeError:
+            pass
         _configured = True
     return L
 
@@ -738,6 +743,24 @@ class Engine:
         cb = PEER_CB(tramp)
         self._keep["peers"] = (t0, t1, cb)
         _check(lib().ktg_engine_set_peers(self._h, rank, world, t0, t1, cb, None))
+
+    def group_area(self):
+        """(device pointer, bytes) of this engine's peer-group exchange area
+        (ktg_engine_group_area); share it with the peers (ipc_handle)."""
+        a, b = _vp(), _u64()
+        _check(lib().ktg_engine_group_area(self._h, ctypes.byref(a), ctypes.byref(b)))
+        return a.value, int(b.value)
+
+    def set_group(self, rank: int, world: int, areas, s0, s1) -> None:
+        """Device-resident partitioned fixpoint (ktg_engine_set_group): every
+        rank's exchange area and support buffers, mapped into this process,
+        own entries at `rank`. Collective; meet in a host barrier before the
+        first run."""
+        ta = (ctypes.c_void_p * world)(*areas)
+        t0 = (ctypes.c_void_p * world)(*s0)
+        t1 = (ctypes.c_void_p * world)(*s1)
+        self._keep["group"] = (ta, t0, t1)
+        _check(lib().ktg_engine_set_group(self._h, rank, world, ta, t0, t1))
 
     def set_partition(self, rank: int, world: int, allreduce=None) -> None:
         cb = ALLREDUCE_CB(allreduce) if allreduce is not None else ALLREDUCE_CB()

@@ -15,8 +15,8 @@ ap.add_argument("--tag", default=os.environ.get("KTG_LIB_DIR", "lib"))
 a = ap.parse_args()
 if not os.path.exists(a.cache):
     g = kt.rmat(a.scale)
-    kt.write_csr_cache(g, a.cache)
-g = kt.read_csr_cache(a.cache)
+    kt.graph.write_csr_cache(g, a.cache)
+g = kt.graph.read_csr_cache(a.cache)
 out = {"tag": a.tag}
 e = kt.Engine(g, kt.TrussOptions(no_degree_bound=True), time_support=True)
 best = 1e9

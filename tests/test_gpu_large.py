@@ -95,23 +95,25 @@ def test_incremental_runs_equal_pristine(s14):
         assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1]), k
 
 
-def test_virtual_gpus_partition_sums_to_full(s14):
-    """Multi-GPU split simulated on one device: the partial
-    supports of P disjoint task shares sum to the full supports."""
+def test_partitioned_engine_support_pass_is_whole_graph(s14):
+    """A standalone support pass (compute_supports / the kmax_search bound,
+    support.cpp:93-132) on an engine partitioned over P ranks is never split
+    (ADVICE r1): every rank returns the whole-graph T and S, so a partitioned
+    kmax cannot bisect under a partial max S. The split itself (partial
+    supports summing to the full ones) is exercised by the multi-rank
+    fixpoint tests (test_gpu_peers.py, test_gpu_group.py)."""
     full = kt.Engine(s14)
     full.reset()
     t_full = full.support_pass()
     S_full = full.read()[1]
     for P in (2, 3, 8):
-        acc = np.zeros_like(S_full, dtype=np.uint64)
-        tri = 0
         for r in range(P):
             e = kt.Engine(s14)
             e.set_partition(r, P, allreduce=lambda *a: 0)
             e.reset()
-            tri += e.support_pass()
-            acc += e.read()[1]
-        assert tri == t_full and np.array_equal(acc.astype(np.uint32), S_full), P
+            assert e.support_pass() == t_full, (P, r)
+            assert np.array_equal(e.read()[1], S_full), (P, r)
+            e.close()
 
 
 def test_skew_graph(port):
@@ -167,17 +169,31 @@ def test_s20_byte_exact(s20, port, k, mode, monkeypatch):
 
 
 def test_rank_partials_match_oracle_task_partition(port):
-    """Each rank's partial supports (device task share t % world == rank)
-    equal the oracle's mirror of the device planner, rank by rank."""
+    """Each rank's partial supports of a partitioned fixpoint's first round
+    (recompute path: work-balanced chunk range + off-diagonal share) equal
+    the oracle's mirror of the device planner, rank by rank. The partial
+    buffer is captured inside the allreduce callback, before any exchange."""
+    import ctypes
     g = kt.rmat(12, 16, seed=9)
     for world in (2, 3):
         for r in range(world):
+            got = []
+
+            def cb(d_buf, count, stream, user):
+                if not got:
+                    host = np.empty(count, np.uint32)
+                    kt.truss.device_copy(host.ctypes.data, ctypes.cast(d_buf, ctypes.c_void_p).value, 4 * count,
+                                         stream)
+                    got.append(host)
+                return 0
+
             e = kt.Engine(g, kt.TrussOptions(label_order=True))
-            e.set_partition(r, world, allreduce=lambda *a: 0)
+            e.set_partition(r, world, allreduce=cb)
             e.reset()
-            t = e.support_pass()
+            e.run(3)
+            e.close()
             t_o, S_o = port.support_tasks(g, r, world, chunk=kt.truss.lib().ktg_task_chunk())
-            assert t == t_o and np.array_equal(e.read()[1], S_o), (world, r)
+            assert np.array_equal(got[0], S_o), (world, r)
 
 
 def test_nccl_single_rank_fixpoint(port):
