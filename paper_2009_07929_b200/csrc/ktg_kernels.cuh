@@ -839,11 +839,18 @@ k_support_chunked(Graph g) {
 #define KTG_A22_UNROLL 4
 #endif
 constexpr int kA22Batch = 256;
-#ifndef KTG_A22_GROUP
-#define KTG_A22_GROUP 8
+#ifndef KTG_A22_LIGHT
+#define KTG_A22_LIGHT 1    // round-0 light pivots skip their increments
 #endif
-constexpr int kA22Group = KTG_A22_GROUP;   // batches of one chunk per task (staged once)
-constexpr int kA22TableBits = 11;          // 2048 slots for <= 512 entries (load <= 0.25)
+#ifndef KTG_A22_QUEUE
+#define KTG_A22_QUEUE 1
+#endif
+#ifndef KTG_A22_TABLE_BITS
+#define KTG_A22_TABLE_BITS (KTG_A22_QUEUE ? 10 : 11)
+#endif
+// table slots for <= 512 entries: 1024 (load <= 0.5) with the positive queue
+// (probes run on full warps; keeps smem at 6 CTAs / SM), else 2048
+constexpr int kA22TableBits = KTG_A22_TABLE_BITS;
 constexpr int kA22Strip = 256;             // flat tail elements a warp takes per grab
 constexpr int kA22Table = 1 << kA22TableBits;
 constexpr int kA22Unroll = KTG_A22_UNROLL;     // tail elements per lane per step (loads in flight)
@@ -870,6 +877,11 @@ struct A22Smem {
   uint32_t pref[kA22Batch + 1];
   uint32_t filt[kA22FiltWords];      // membership bits of (value, run end): most misses stop here
   uint2 tab[kA22Table];              // open addressing: {value (0 = empty), chunk position}
+#if KTG_A22_QUEUE
+  uint32_t qc[kSupportThreads / 32][32 * kA22Unroll];  // per-warp filter positives: value,
+  uint32_t qs[kSupportThreads / 32][32 * kA22Unroll];  //   tail slot,
+  uint32_t qr[kSupportThreads / 32][32 * kA22Unroll];  //   packed run / pivot / light
+#endif
   uint32_t red[kSupportThreads / 32];
   uint32_t task;
   uint32_t next;
@@ -884,14 +896,11 @@ __device__ __forceinline__ uint32_t a22_slot(uint32_t h) { return h >> (32 - kA2
 __device__ __forceinline__ uint32_t a22_fbit(uint32_t h) { return (h ^ (h >> 15)) & (kA22FiltWords * 32 - 1); }
 
 // COST = true (multi-rank runs, before every full pass): steps 1-2 only, over
-// all tasks; cost[t] = the task's flattened tail work W, the weights of the
+// all tasks; wcost[t] = the task's flattened tail work W, the weights of the
 // work-balanced split of the tasks across ranks (k_a22_split).
-#ifndef KTG_A22_MINB
-#define KTG_A22_MINB 6
-#endif
 template <bool COST>
-__global__ void __launch_bounds__(kSupportThreads, KTG_A22_MINB)
-k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ cost) {
+__global__ void __launch_bounds__(kSupportThreads, 6)  // 6 CTAs/SM (smem-bound): <= 40 registers
+k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ wcost) {
   if (g.st->mode) return;  // supports carried this round
   // static (not dynamic) shared memory: constant-offset LDS addressing
   __shared__ __align__(16) A22Smem s;
@@ -903,18 +912,19 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ cost) {
   const uint32_t* __restrict__ col = g.col;
   const uint32_t h0 = g.st->h0;
   const bool pristine = g.st->pristine;
-  // multi-rank runs: this rank's contiguous, work-balanced range of tasks
-  const uint32_t t_lo = (g.world > 1 && !COST) ? g.st->a22_lo : 0u;
-  const uint32_t t_hi = (g.world > 1 && !COST) ? g.st->a22_hi : a.ntasks;
-  unsigned long long task_w = 0;
   unsigned long long tri_local = 0;
 
   for (;;) {
-    if (tid == 0) s.task = atomicAdd(&g.st->task_next, 1u);
+    if (tid == 0) {
+      // multi-rank runs: this rank's contiguous, work-balanced task range
+      const bool part = g.world > 1 && !COST;
+      const uint32_t tt = atomicAdd(&g.st->task_next, 1u) + (part ? g.st->a22_lo : 0u);
+      s.task = tt < (part ? g.st->a22_hi : a.ntasks) ? tt : 0xffffffffu;
+      s.next = 0;
+    }
     __syncthreads();
-    const uint32_t t = t_lo + s.task;
-    if (t >= t_hi) break;
-    task_w = 0;
+    const uint32_t t = s.task;
+    if (t == 0xffffffffu) break;
     const uint2 tk = a.tasks[a.ntasks - 1 - t];  // dense (high-rank) chunks first
     const uint32_t q = tk.x;
     const uint64_t a0 = (uint64_t)q * kChunk;
@@ -922,9 +932,9 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ cost) {
     const uint32_t jf = a.jfirst[q], jl = g.chunk_row[q];
     const uint32_t nrows = jl - jf + 1;
 
-    // 1. rows of the chunk (live run inside the chunk, in-list offsets),
-    //    once per task: a task is up to kA22Group consecutive batches of the
-    //    same chunk, so the chunk is staged once for all of them
+    // 1. rows of the chunk (live run inside the chunk, in-list offsets) and
+    //    the batch's pivot descriptors, before anything is staged: batches
+    //    whose pivots are all dead cost only this
     for (uint32_t r = tid; r <= nrows; r += kSupportThreads) {
       const uint32_t j = jf + r;
       s.roff[r] = a.pin_off[j];
@@ -935,217 +945,254 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ cost) {
       }
     }
     __syncthreads();
-    const uint32_t kbeg = s.roff[0], kend = s.roff[nrows];
-    const uint32_t ylim = min(tk.y + (uint32_t)kA22Group, (kend - kbeg + kA22Batch - 1) / kA22Batch);
-    bool staged = false;  // block-uniform
 
-    for (uint32_t yb = tk.y; yb < ylim; ++yb) {
-      // 2. pivot descriptors of this batch: slot, tail (clipped to the run's
-      //    value range when j's row continues outside the chunk)
-      const uint32_t k0 = kbeg + yb * kA22Batch;
-      const uint32_t k1 = min(k0 + kA22Batch, kend);
-      uint32_t cost = 0;
-      s.cntP[tid] = 0;
-      if (tid == 0) s.next = 0;
-      if (k0 + tid < k1) {
-        const uint32_t k = k0 + tid;
-        // row of pivot k: last r with roff[r] <= k
-        uint32_t lo = 0, hi = nrows;
-        while (hi - lo > 1) {
-          const uint32_t mid = (lo + hi) >> 1;
-          if (s.roff[mid] <= k) lo = mid; else hi = mid;
-        }
-        const uint32_t run = s.rte[lo];
-        bool live = false;
-        uint32_t ps = 0, i = 0;
-        if (run != 0xffffffffu) {
-          if (pristine) {  // static {slot, row}: no dead / pos_of / erow gathers
-            const uint2 pv = a.pin_p[k];
-            ps = pv.x, i = pv.y, live = true;
-          } else {
-            const uint32_t id = a.pe[k];
-            live = !y.dead[id];
-            if (live) ps = y.pos_of[id], i = y.erow[id];
-          }
-        }
-        if (live) {
-          const uint32_t iend = g.row_ptr[i] + g.deg[i];
-          uint32_t tlo = ps + 1, thi = iend;
-          const uint32_t tb = run >> 16, te = run & 0xffffu;
-          const uint32_t j = jf + lo;
-          const uint64_t rb = g.row_ptr[j];
-          if (rb < a0 || rb + g.deg[j] > a0 + alen) {  // partial run: clip the tail
-            tlo = lb_global(col, tlo, thi, col[a0 + tb]);
-            thi = lb_global(col, tlo, thi, col[a0 + te - 1] + 1);
-          }
-          if (thi > tlo) {
-            cost = thi - tlo;
-            // pristine round 0 with the degree bound: rows below h0 go in
-            // this round whatever their counts (k_mark), so their slots --
-            // the pivot (i, j) and its tail (i, c) -- need no increments;
-            // bit 31 of the run marks such a pivot
-            const bool light = i < h0;
-            s.ps[tid] = light ? 0xffffffffu : ps;
-            s.plo[tid] = tlo;
-            s.prun[tid] = run | (light ? 0x80000000u : 0u);
-          }
+    // 2. pivot descriptors of this batch: slot, tail (clipped to the run's
+    //    value range when j's row continues outside the chunk)
+    const uint32_t k0 = s.roff[0] + tk.y * kA22Batch;
+    const uint32_t k1 = min(k0 + kA22Batch, s.roff[nrows]);
+    uint32_t cost = 0;
+    s.cntP[tid] = 0;
+    if (k0 + tid < k1) {
+      const uint32_t k = k0 + tid;
+      // row of pivot k: last r with roff[r] <= k
+      uint32_t lo = 0, hi = nrows;
+      while (hi - lo > 1) {
+        const uint32_t mid = (lo + hi) >> 1;
+        if (s.roff[mid] <= k) lo = mid; else hi = mid;
+      }
+      const uint32_t run = s.rte[lo];
+      bool live = false;
+      uint32_t ps = 0, i = 0;
+      if (run != 0xffffffffu) {
+        if (pristine) {  // static {slot, row}: no dead / pos_of / erow gathers
+          const uint2 pv = a.pin_p[k];
+          ps = pv.x, i = pv.y, live = true;
+        } else {
+          const uint32_t id = a.pe[k];
+          live = !y.dead[id];
+          if (live) ps = y.pos_of[id], i = y.erow[id];
         }
       }
-      uint32_t W;
-      const uint32_t run0 = block_exscan(cost, s.red, &W);
-      s.pref[tid] = run0;
-      if (tid == 0) s.pref[kA22Batch] = W;
-      if (COST) {
-        task_w += W;
-        __syncthreads();  // s.red / s.pref reused by the next batch
-        continue;
-      }
-      if (W == 0) continue;  // no live pivot of this batch reaches the chunk (uniform)
-
-      // 3. first non-empty batch: stage the chunk, next zeros, (value, run
-      //    end) hash -- as k_support_chunked
-      if (!staged) {
-        staged = true;
-        for (uint32_t b = tid; b < (uint32_t)kA22Table; b += kSupportThreads) s.tab[b] = make_uint2(0, 0);
-        for (uint32_t b = tid; b < (uint32_t)kA22FiltWords; b += kSupportThreads) s.filt[b] = 0;
-        uint32_t first_zero = 0xffffffffu;
-#pragma unroll
-        for (int e = 0; e < EPT; ++e) {
-          const uint32_t x = tid * EPT + e;
-          const uint32_t v = x < alen ? col[a0 + x] : 0u;
-          s.A[x] = v;
-          s.cntA[x] = 0;
-          if (v == 0 && x < alen && first_zero == 0xffffffffu) first_zero = x;
+      if (live) {
+        const uint32_t iend = g.row_ptr[i] + g.deg[i];
+        uint32_t tlo = ps + 1, thi = iend;
+        const uint32_t tb = run >> 16, te = run & 0xffffu;
+        const uint32_t j = jf + lo;
+        const uint64_t rb = g.row_ptr[j];
+        if (rb < a0 || rb + g.deg[j] > a0 + alen) {  // partial run: clip the tail
+          tlo = lb_global(col, tlo, thi, col[a0 + tb]);
+          thi = lb_global(col, tlo, thi, col[a0 + te - 1] + 1);
         }
-        uint32_t m = first_zero;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-          const uint32_t v = __shfl_down_sync(0xffffffffu, m, o);
-          if (lane + o < 32) m = min(m, v);
+        if (thi > tlo) {
+          cost = thi - tlo;
+          s.ps[tid] = ps;
+          s.plo[tid] = tlo;
+          // pristine round 0 with the degree bound: rows below h0 go in this
+          // round whatever their counts (k_mark), so the pivot (i, j) and its
+          // tail slots (i, c) need no increments; bit 31 of the run marks it
+          s.prun[tid] = run | ((KTG_A22_LIGHT && i < h0) ? 0x80000000u : 0u);
         }
-        if (lane == 0) s.red[wid] = m;
-        __syncthreads();
-        uint32_t carry = 0xffffffffu;
-        for (int w = wid + 1; w < NW; ++w) carry = min(carry, s.red[w]);
-        const uint32_t incl_next = __shfl_down_sync(0xffffffffu, m, 1);
-        if (lane < 31) carry = min(carry, incl_next);
-        uint32_t cur = min(carry, alen);
-#pragma unroll
-        for (int e = EPT - 1; e >= 0; --e) {
-          const uint32_t x = tid * EPT + e;
-          const uint32_t v = s.A[x];
-          if (x < alen && v == 0) cur = x;
-          if (v != 0) {  // claim the first free slot from home (values are >= 1)
-            const uint32_t hh = a22_mix(v, cur);
-            const uint32_t fb = a22_fbit(hh);
-            atomicOr(&s.filt[fb >> 5], 1u << (fb & 31));
-            uint32_t h = a22_slot(hh);
-            while (atomicCAS(&s.tab[h].x, 0u, v) != 0u) h = (h + 1) & (kA22Table - 1);
-            s.tab[h].y = x;
-          }
-        }
-      }
-      __syncthreads();
-
-      // 4. flattened tail elements, strips grabbed dynamically by warps
-      uint32_t tri_task = 0;
-      // pivot counts accumulate per lane while its pivot stays the same (a
-      // lane's pivot index only grows) and go to smem once per change
-      uint32_t accP = 0, accN = 0;
-      for (;;) {
-        uint32_t base = 0;
-        if (lane == 0) base = atomicAdd(&s.next, (uint32_t)kA22Strip);
-        base = __shfl_sync(0xffffffffu, base, 0);
-        if (base >= W) break;
-        const uint32_t lim = min(base + (uint32_t)kA22Strip, W);
-        // pivot holding base: p = #{q in [1, kA22Batch) : pref[q] <= base}
-        // (pref ascends), two ballots over groups of 8 instead of a search
-        static_assert(kA22Batch == 256, "two-level ballot assumes 32 groups of 8");
-        uint32_t p;
-        {
-          const uint32_t g8 = __popc(__ballot_sync(0xffffffffu, lane < 31 && s.pref[8 * (lane + 1)] <= base));
-          const uint32_t c2 = __popc(__ballot_sync(0xffffffffu, lane < 7 && s.pref[8 * g8 + 1 + lane] <= base));
-          p = 8 * g8 + c2;
-        }
-        uint32_t pe_ = s.pref[p + 1], pb = s.pref[p], plo = s.plo[p], prun = s.prun[p];
-        // (value, run) lookup of tail element c of pivot pp: the value may also
-        // sit in other rows' runs
-        auto probe = [&](uint32_t c, uint32_t slot, uint32_t run, uint32_t pp) {
-          const uint32_t tb = (run >> 16) & 0x7fffu, te = run & 0xffffu;
-          const uint32_t hh = a22_mix(c, te);
-          const uint32_t fb = a22_fbit(hh);
-          if (s.filt[fb >> 5] & (1u << (fb & 31))) {
-            uint32_t x = kChunk;
-            for (uint32_t h = a22_slot(hh);; h = (h + 1) & (kA22Table - 1)) {
-              const uint2 e = s.tab[h];
-              if (e.x == 0) break;
-              if (e.x == c && e.y - tb < te - tb) {
-                x = e.y;
-                break;
-              }
-            }
-            if (x < (uint32_t)kChunk) {
-              atomicAdd(&s.cntA[x], 1u);
-              if (!(run >> 31)) {
-                atomicAdd(&S[slot], 1u);
-                if (pp != accP) {
-                  if (accN) atomicAdd(&s.cntP[accP], accN);
-                  accP = pp;
-                  accN = 0;
-                }
-                ++accN;
-              }
-              ++tri_task;
-            }
-          }
-        };
-        auto advance = [&](uint32_t f) {
-          if (f >= pe_) {
-            do {
-              ++p;
-              pe_ = s.pref[p + 1];
-            } while (pe_ <= f);
-            pb = s.pref[p];
-            plo = s.plo[p];
-            prun = s.prun[p];
-          }
-        };
-        // kA22Unroll elements per lane per step, every load issued before any probe
-        for (uint32_t f = base + lane; f < lim; f += 32 * kA22Unroll) {
-          uint32_t sl[kA22Unroll], ru[kA22Unroll], pv[kA22Unroll], cv[kA22Unroll];
-#pragma unroll
-          for (int u = 0; u < kA22Unroll; ++u) {
-            const uint32_t fu = f + 32 * u;
-            if (fu < lim) advance(fu);
-            sl[u] = plo + (fu - pb), ru[u] = prun, pv[u] = p;
-          }
-#pragma unroll
-          for (int u = 0; u < kA22Unroll; ++u) cv[u] = (f + 32 * u < lim) ? col[sl[u]] : 0u;
-#pragma unroll
-          for (int u = 0; u < kA22Unroll; ++u)
-            if (f + 32 * u < lim) probe(cv[u], sl[u], ru[u], pv[u]);
-        }
-      }
-      if (accN) atomicAdd(&s.cntP[accP], accN);
-      tri_local += tri_task;
-      __syncthreads();
-
-      // 5a. flush this batch's pivot counts (the next batch reuses the slots)
-      {
-        const uint32_t cp = s.cntP[tid];
-        if (cp) atomicAdd(&S[s.ps[tid]], cp);  // light pivots never count (cp = 0)
       }
     }
+    uint32_t W;
+    const uint32_t run0 = block_exscan(cost, s.red, &W);
+    s.pref[tid] = run0;
+    if (tid == 0) s.pref[kA22Batch] = W;
+    if (COST) {
+      if (tid == 0) wcost[t] = W;
+      continue;
+    }
+    if (W == 0) continue;  // no live pivot reaches this chunk (uniform; nothing staged yet)
 
-    if (COST && tid == 0) cost[t] = task_w;
-    // 5b. flush the staged chunk's A22 counts once per task
-    if (staged) {
+    // 3. stage the chunk, next zeros, (value, run end) hash -- as k_support_chunked
+    for (uint32_t b = tid; b < (uint32_t)kA22Table; b += kSupportThreads) s.tab[b] = make_uint2(0, 0);
+    for (uint32_t b = tid; b < (uint32_t)kA22FiltWords; b += kSupportThreads) s.filt[b] = 0;
+    uint32_t first_zero = 0xffffffffu;
 #pragma unroll
-      for (int e = 0; e < EPT; ++e) {
-        const uint32_t x = tid * EPT + e;
-        const uint32_t ca = s.cntA[x];
-        if (ca) atomicAdd(&S[a0 + x], ca);
+    for (int e = 0; e < EPT; ++e) {
+      const uint32_t x = tid * EPT + e;
+      const uint32_t v = x < alen ? col[a0 + x] : 0u;
+      s.A[x] = v;
+      s.cntA[x] = 0;
+      if (v == 0 && x < alen && first_zero == 0xffffffffu) first_zero = x;
+    }
+    {
+      uint32_t m = first_zero;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_down_sync(0xffffffffu, m, o);
+        if (lane + o < 32) m = min(m, v);
       }
+      if (lane == 0) s.red[wid] = m;
+      __syncthreads();
+      uint32_t carry = 0xffffffffu;
+      for (int w = wid + 1; w < NW; ++w) carry = min(carry, s.red[w]);
+      const uint32_t incl_next = __shfl_down_sync(0xffffffffu, m, 1);
+      if (lane < 31) carry = min(carry, incl_next);
+      uint32_t cur = min(carry, alen);
+#pragma unroll
+      for (int e = EPT - 1; e >= 0; --e) {
+        const uint32_t x = tid * EPT + e;
+        const uint32_t v = s.A[x];
+        if (x < alen && v == 0) cur = x;
+        if (v != 0) {  // claim the first free slot from home (values are >= 1)
+          const uint32_t hh = a22_mix(v, cur);
+          const uint32_t fb = a22_fbit(hh);
+          atomicOr(&s.filt[fb >> 5], 1u << (fb & 31));
+          uint32_t h = a22_slot(hh);
+          while (atomicCAS(&s.tab[h].x, 0u, v) != 0u) h = (h + 1) & (kA22Table - 1);
+          s.tab[h].y = x;
+        }
+      }
+    }
+    __syncthreads();
+
+    // 4. flattened tail elements, strips grabbed dynamically by warps
+    uint32_t tri_task = 0;
+    for (;;) {
+      uint32_t base = 0;
+      if (lane == 0) base = atomicAdd(&s.next, (uint32_t)kA22Strip);
+      base = __shfl_sync(0xffffffffu, base, 0);
+      if (base >= W) break;
+      const uint32_t lim = min(base + (uint32_t)kA22Strip, W);
+      // pivot holding base: p = #{q in [1, kA22Batch) : pref[q] <= base}
+      // (pref ascends), two ballots over groups of 8 instead of a search
+      static_assert(kA22Batch == 256, "two-level ballot assumes 32 groups of 8");
+      uint32_t p;
+      {
+        const uint32_t g = __popc(__ballot_sync(0xffffffffu, lane < 31 && s.pref[8 * (lane + 1)] <= base));
+        const uint32_t c2 = __popc(__ballot_sync(0xffffffffu, lane < 7 && s.pref[8 * g + 1 + lane] <= base));
+        p = 8 * g + c2;
+      }
+      uint32_t pe_ = s.pref[p + 1], pb = s.pref[p], plo = s.plo[p], prun = s.prun[p];
+      // (value, run) lookup of tail element c of pivot pp: the value may also
+      // sit in other rows' runs
+      auto probe = [&](uint32_t c, uint32_t slot, uint32_t run, uint32_t pp) {
+        const uint32_t tb = (run >> 16) & 0x7fffu, te = run & 0xffffu;
+        const uint32_t hh = a22_mix(c, te);
+        const uint32_t fb = a22_fbit(hh);
+        if (s.filt[fb >> 5] & (1u << (fb & 31))) {
+          uint32_t x = kChunk;
+          for (uint32_t h = a22_slot(hh);; h = (h + 1) & (kA22Table - 1)) {
+            const uint2 e = s.tab[h];
+            if (e.x == 0) break;
+            if (e.x == c && e.y - tb < te - tb) {
+              x = e.y;
+              break;
+            }
+          }
+          if (x < (uint32_t)kChunk) {
+            atomicAdd(&s.cntA[x], 1u);
+            if (!KTG_A22_LIGHT || !(run >> 31)) {
+              atomicAdd(&S[slot], 1u);
+              atomicAdd(&s.cntP[pp], 1u);
+            }
+            ++tri_task;
+          }
+        }
+      };
+      auto advance = [&](uint32_t f) {
+        if (f >= pe_) {
+          do {
+            ++p;
+            pe_ = s.pref[p + 1];
+          } while (pe_ <= f);
+          pb = s.pref[p];
+          plo = s.plo[p];
+          prun = s.prun[p];
+        }
+      };
+#if KTG_A22_QUEUE
+      // kA22Unroll elements per lane per step, every load issued before any
+      // test; filter positives (~hits, 25% of the elements at R-MAT s24) are
+      // queued per warp in element order and confirmed by the table with
+      // all 32 lanes busy, instead of each positive stalling its warp
+      uint32_t* __restrict__ qc = s.qc[wid];
+      uint32_t* __restrict__ qs = s.qs[wid];
+      uint32_t* __restrict__ qr = s.qr[wid];
+      for (uint32_t f0 = base; f0 < lim; f0 += 32 * kA22Unroll) {  // warp-uniform trips
+        const uint32_t f = f0 + lane;
+        uint32_t sl[kA22Unroll], ru[kA22Unroll], pv[kA22Unroll], cv[kA22Unroll];
+#pragma unroll
+        for (int u = 0; u < kA22Unroll; ++u) {
+          const uint32_t fu = f + 32 * u;
+          if (fu < lim) advance(fu);
+          sl[u] = plo + (fu - pb), ru[u] = prun, pv[u] = p;
+        }
+#pragma unroll
+        for (int u = 0; u < kA22Unroll; ++u) cv[u] = (f + 32 * u < lim) ? col[sl[u]] : 0u;
+        uint32_t nq = 0;
+#pragma unroll
+        for (int u = 0; u < kA22Unroll; ++u) {
+          const uint32_t run = ru[u];
+          const uint32_t te = run & 0xffffu;
+          const uint32_t fb = a22_fbit(a22_mix(cv[u], te));
+          const bool pos = (f + 32 * u < lim) && (s.filt[fb >> 5] & (1u << (fb & 31)));
+          const uint32_t m = __ballot_sync(0xffffffffu, pos);
+          if (pos) {
+            const uint32_t at = nq + __popc(m & ((1u << lane) - 1u));
+            qc[at] = cv[u];
+            qs[at] = sl[u];
+            // run te (10 bits) | tb (10 bits) << 10 | pivot << 20 | light bit 31
+            qr[at] = te | (((run >> 16) & 0x3ffu) << 10) | (pv[u] << 20) | (run & 0x80000000u);
+          }
+          nq += __popc(m);
+        }
+        __syncwarp();
+        for (uint32_t e = lane; e < nq; e += 32) {
+          const uint32_t c = qc[e], slot = qs[e], r = qr[e];
+          const uint32_t te = r & 0x3ffu, tb = (r >> 10) & 0x3ffu;
+          uint32_t x = kChunk;
+          for (uint32_t h = a22_slot(a22_mix(c, te));; h = (h + 1) & (kA22Table - 1)) {
+            const uint2 en = s.tab[h];
+            if (en.x == 0) break;
+            if (en.x == c && en.y - tb < te - tb) {
+              x = en.y;
+              break;
+            }
+          }
+          if (x < (uint32_t)kChunk) {
+            atomicAdd(&s.cntA[x], 1u);
+            if (!KTG_A22_LIGHT || !(r >> 31)) {
+              atomicAdd(&S[slot], 1u);
+              atomicAdd(&s.cntP[(r >> 20) & 0xffu], 1u);
+            }
+            ++tri_task;
+          }
+        }
+        __syncwarp();
+      }
+#else
+      // kA22Unroll elements per lane per step, every load issued before any probe
+      for (uint32_t f = base + lane; f < lim; f += 32 * kA22Unroll) {
+        uint32_t sl[kA22Unroll], ru[kA22Unroll], pv[kA22Unroll], cv[kA22Unroll];
+#pragma unroll
+        for (int u = 0; u < kA22Unroll; ++u) {
+          const uint32_t fu = f + 32 * u;
+          if (fu < lim) advance(fu);
+          sl[u] = plo + (fu - pb), ru[u] = prun, pv[u] = p;
+        }
+#pragma unroll
+        for (int u = 0; u < kA22Unroll; ++u) cv[u] = (f + 32 * u < lim) ? col[sl[u]] : 0u;
+#pragma unroll
+        for (int u = 0; u < kA22Unroll; ++u)
+          if (f + 32 * u < lim) probe(cv[u], sl[u], ru[u], pv[u]);
+      }
+#endif
+    }
+    tri_local += tri_task;
+    __syncthreads();
+
+    // 5. flush shared counts (A22 slots, pivots)
+#pragma unroll
+    for (int e = 0; e < EPT; ++e) {
+      const uint32_t x = tid * EPT + e;
+      const uint32_t ca = s.cntA[x];
+      if (ca) atomicAdd(&S[a0 + x], ca);
+    }
+    {
+      const uint32_t cp = s.cntP[tid];
+      if (cp) atomicAdd(&S[s.ps[tid]], cp);
     }
     __syncthreads();
   }
@@ -1168,8 +1215,7 @@ __global__ void k_chunk_first(const uint32_t* __restrict__ row_ptr, uint32_t n, 
   jfirst[q] = max(lo - 1, 1u);
 }
 
-// Load time: tasks per chunk (batches of kA22Batch pivots into the chunk's
-// rows, kA22Group batches per task).
+// Load time: batches per chunk (pivots into the chunk's rows / kA22Batch).
 __global__ void k_a22_count(const uint32_t* __restrict__ jfirst, const uint32_t* __restrict__ chunk_row,
                             const uint32_t* __restrict__ pin_off, uint32_t nchunks, uint32_t* __restrict__ cnt) {
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
@@ -1179,15 +1225,14 @@ __global__ void k_a22_count(const uint32_t* __restrict__ jfirst, const uint32_t*
     return;
   }
   const uint32_t k0 = pin_off[jfirst[q]], k1 = pin_off[chunk_row[q] + 1];
-  const uint32_t nb = (k1 - k0 + kA22Batch - 1) / kA22Batch;
-  cnt[q] = (nb + kA22Group - 1) / kA22Group;
+  cnt[q] = (k1 - k0 + kA22Batch - 1) / kA22Batch;
 }
 
 __global__ void k_a22_fill(const uint32_t* __restrict__ cnt_off, uint32_t nchunks, uint2* __restrict__ tasks) {
   const uint32_t q = blockIdx.x * blockDim.x + threadIdx.x;
   if (q >= nchunks) return;
   const uint32_t o = cnt_off[q], c = cnt_off[q + 1] - o;
-  for (uint32_t b = 0; b < c; ++b) tasks[o + b] = make_uint2(q, b * kA22Group);
+  for (uint32_t b = 0; b < c; ++b) tasks[o + b] = make_uint2(q, b);
 }
 
 // Multi-rank full pass: rank r takes the contiguous tasks
