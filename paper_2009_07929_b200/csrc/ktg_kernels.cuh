@@ -842,15 +842,7 @@ constexpr int kA22Batch = 256;
 #ifndef KTG_A22_LIGHT
 #define KTG_A22_LIGHT 1    // round-0 light pivots skip their increments
 #endif
-#ifndef KTG_A22_QUEUE
-#define KTG_A22_QUEUE 1
-#endif
-#ifndef KTG_A22_TABLE_BITS
-#define KTG_A22_TABLE_BITS (KTG_A22_QUEUE ? 10 : 11)
-#endif
-// table slots for <= 512 entries: 1024 (load <= 0.5) with the positive queue
-// (probes run on full warps; keeps smem at 6 CTAs / SM), else 2048
-constexpr int kA22TableBits = KTG_A22_TABLE_BITS;
+constexpr int kA22TableBits = 11;          // 2048 slots for <= 512 entries (load <= 0.25)
 constexpr int kA22Strip = 256;             // flat tail elements a warp takes per grab
 constexpr int kA22Table = 1 << kA22TableBits;
 constexpr int kA22Unroll = KTG_A22_UNROLL;     // tail elements per lane per step (loads in flight)
@@ -877,11 +869,6 @@ struct A22Smem {
   uint32_t pref[kA22Batch + 1];
   uint32_t filt[kA22FiltWords];      // membership bits of (value, run end): most misses stop here
   uint2 tab[kA22Table];              // open addressing: {value (0 = empty), chunk position}
-#if KTG_A22_QUEUE
-  uint32_t qc[kSupportThreads / 32][32 * kA22Unroll];  // per-warp filter positives: value,
-  uint32_t qs[kSupportThreads / 32][32 * kA22Unroll];  //   tail slot,
-  uint32_t qr[kSupportThreads / 32][32 * kA22Unroll];  //   packed run / pivot / light
-#endif
   uint32_t red[kSupportThreads / 32];
   uint32_t task;
   uint32_t next;
@@ -1102,67 +1089,6 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ wcost) {
           prun = s.prun[p];
         }
       };
-#if KTG_A22_QUEUE
-      // kA22Unroll elements per lane per step, every load issued before any
-      // test; filter positives (~hits, 25% of the elements at R-MAT s24) are
-      // queued per warp in element order and confirmed by the table with
-      // all 32 lanes busy, instead of each positive stalling its warp
-      uint32_t* __restrict__ qc = s.qc[wid];
-      uint32_t* __restrict__ qs = s.qs[wid];
-      uint32_t* __restrict__ qr = s.qr[wid];
-      for (uint32_t f0 = base; f0 < lim; f0 += 32 * kA22Unroll) {  // warp-uniform trips
-        const uint32_t f = f0 + lane;
-        uint32_t sl[kA22Unroll], ru[kA22Unroll], pv[kA22Unroll], cv[kA22Unroll];
-#pragma unroll
-        for (int u = 0; u < kA22Unroll; ++u) {
-          const uint32_t fu = f + 32 * u;
-          if (fu < lim) advance(fu);
-          sl[u] = plo + (fu - pb), ru[u] = prun, pv[u] = p;
-        }
-#pragma unroll
-        for (int u = 0; u < kA22Unroll; ++u) cv[u] = (f + 32 * u < lim) ? col[sl[u]] : 0u;
-        uint32_t nq = 0;
-#pragma unroll
-        for (int u = 0; u < kA22Unroll; ++u) {
-          const uint32_t run = ru[u];
-          const uint32_t te = run & 0xffffu;
-          const uint32_t fb = a22_fbit(a22_mix(cv[u], te));
-          const bool pos = (f + 32 * u < lim) && (s.filt[fb >> 5] & (1u << (fb & 31)));
-          const uint32_t m = __ballot_sync(0xffffffffu, pos);
-          if (pos) {
-            const uint32_t at = nq + __popc(m & ((1u << lane) - 1u));
-            qc[at] = cv[u];
-            qs[at] = sl[u];
-            // run te (10 bits) | tb (10 bits) << 10 | pivot << 20 | light bit 31
-            qr[at] = te | (((run >> 16) & 0x3ffu) << 10) | (pv[u] << 20) | (run & 0x80000000u);
-          }
-          nq += __popc(m);
-        }
-        __syncwarp();
-        for (uint32_t e = lane; e < nq; e += 32) {
-          const uint32_t c = qc[e], slot = qs[e], r = qr[e];
-          const uint32_t te = r & 0x3ffu, tb = (r >> 10) & 0x3ffu;
-          uint32_t x = kChunk;
-          for (uint32_t h = a22_slot(a22_mix(c, te));; h = (h + 1) & (kA22Table - 1)) {
-            const uint2 en = s.tab[h];
-            if (en.x == 0) break;
-            if (en.x == c && en.y - tb < te - tb) {
-              x = en.y;
-              break;
-            }
-          }
-          if (x < (uint32_t)kChunk) {
-            atomicAdd(&s.cntA[x], 1u);
-            if (!KTG_A22_LIGHT || !(r >> 31)) {
-              atomicAdd(&S[slot], 1u);
-              atomicAdd(&s.cntP[(r >> 20) & 0xffu], 1u);
-            }
-            ++tri_task;
-          }
-        }
-        __syncwarp();
-      }
-#else
       // kA22Unroll elements per lane per step, every load issued before any probe
       for (uint32_t f = base + lane; f < lim; f += 32 * kA22Unroll) {
         uint32_t sl[kA22Unroll], ru[kA22Unroll], pv[kA22Unroll], cv[kA22Unroll];
@@ -1178,7 +1104,6 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ wcost) {
         for (int u = 0; u < kA22Unroll; ++u)
           if (f + 32 * u < lim) probe(cv[u], sl[u], ru[u], pv[u]);
       }
-#endif
     }
     tri_local += tri_task;
     __syncthreads();
