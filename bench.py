@@ -365,6 +365,7 @@ def main():
         h = eng.run(k)
         rounds[k] = len(h)
         live[k] = int(eng.info()["live_edges"])
+    carried_mode = bool(eng.info()["carried"])
     kmax_ok = None
     if "kmax" in args.ks and world == 1:  # K_max really is K_max on this graph
         eng.reset()
@@ -511,6 +512,8 @@ def main():
         cfg = base_config(args, ks, n, m, slots)
         cfg.update({
             "k_max": kmax, "k_max_confirmed_on_device": kmax_ok,
+            "engine_mode": "carried supports (default)" if carried_mode else
+                           "recompute every round (carried-support structures do not fit in HBM)",
             "rounds": {str(k): rounds[k] for k in ks} if len(ks) <= 8 else sum(rounds.values()),
             "survivors": {str(k): live[k] for k in ks} if len(ks) <= 8 else None,
             "l2": "512 MiB memset before every fixpoint; col_idx %.0f MB %s L2 (126 MB)" %

@@ -179,6 +179,11 @@ typedef struct {
   uint64_t triangles;        /* triangle total of the converged round        */
   uint32_t max_support;      /* max S of the first round (kmax bound)        */
   double device_ms;          /* CUDA-event time of the last run              */
+  uint32_t carried;          /* 1: supports can be carried across rounds (the
+                                default path's structures are resident); 0:
+                                every round recomputes (KTG_FLAG_RECOMPUTE,
+                                label order, or the carried-support structures
+                                did not fit in device memory at load)       */
 } ktg_run_info;
 
 /* Per-round closed-form work, recorded with KTG_FLAG_COLLECT_WORK. */

@@ -292,6 +292,27 @@ struct ktg_engine {
     return x;
   }
 
+  // The carried-support structures only (symmetric rows, per-edge maps,
+  // frontier / delta queues, A22 plan).
+  void release_sym() {
+    for (DBuf<uint32_t>* b : {&sym_nbr, &sym_eid, &sym_nbr_p, &sym_eid_p, &sym_deg, &sym_deg_p, &pos_of, &pos_of_p,
+                              &erow, &qsym, &qrow, &fq0, &fq1, &sym_heavy, &a22_pe, &a22_off, &a22_jfirst,
+                              &a22_cnt})
+      b->release();
+    sym_ptr.release();
+    sym_sizes.release();
+    dead.release();
+    rdirty.release();
+    sdirty.release();
+    rq.release();
+    a22_tasks.release();
+    a22_pin.release();
+    a22_cost.release();
+    a22_pre.release();
+    sym_ready = false;
+    a22_ready = false;
+  }
+
   void free_all() {
     if (exec) cudaGraphExecDestroy(exec);
     exec = nullptr;
@@ -734,10 +755,19 @@ ktg_status engine_load(ktg_engine* e, const uint32_t* row_ptr, uint32_t n, const
     // carried-support runs need the symmetric rows (col marks use the top bit)
     const bool with_sym = !flag(e, KTG_FLAG_RECOMPUTE) && n <= 0x7fffffffu;
     e->sym_ready = false;
-    KTG_TRY(build_working(e, with_sym));
+    ktg_status st = build_working(e, with_sym);
     mark("working layout (+ symmetric rows)");
-    if (with_sym) KTG_TRY(build_sym(e));
+    if (st == KTG_OK && with_sym) st = build_sym(e);
     mark("A22 plan");
+    if (st == KTG_ERR_OOM && with_sym) {
+      // the carried-support structures (symmetric rows, per-edge maps, A22
+      // plan, delta queues) do not fit next to the graph: drop them and run
+      // this graph the paper's way, a full support pass every round
+      cudaGetLastError();
+      e->release_sym();
+      st = build_working(e, false);
+    }
+    KTG_TRY(st);
   }
   if (had_group && e->act().S0.p == g_bufs[0] && e->act().S1.p == g_bufs[1] &&
       (void*)e->act().slots == g_bufs[2] && e->xcap >= e->act().live_pristine) {
@@ -1213,6 +1243,7 @@ ktg_status finish_info(ktg_engine* e) {
   e->info.live_edges = e->h_st->live;
   e->info.triangles = e->h_st->last_triangles;
   e->info.device_ms = ms;
+  e->info.carried = (e->reoriented && e->sym_ready && !flag(e, KTG_FLAG_RECOMPUTE)) ? 1u : 0u;
   if (e->h_st->error) return overflow_error(e);
   return KTG_OK;
 }

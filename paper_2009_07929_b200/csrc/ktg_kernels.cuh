@@ -885,8 +885,11 @@ __device__ __forceinline__ uint32_t a22_fbit(uint32_t h) { return (h ^ (h >> 15)
 // COST = true (multi-rank runs, before every full pass): steps 1-2 only, over
 // all tasks; wcost[t] = the task's flattened tail work W, the weights of the
 // work-balanced split of the tasks across ranks (k_a22_split).
+#ifndef KTG_A22_MINB
+#define KTG_A22_MINB 6
+#endif
 template <bool COST>
-__global__ void __launch_bounds__(kSupportThreads, 6)  // 6 CTAs/SM (smem-bound): <= 40 registers
+__global__ void __launch_bounds__(kSupportThreads, KTG_A22_MINB)  // 6 CTAs/SM (smem-bound): <= 40 registers
 k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ wcost) {
   if (g.st->mode) return;  // supports carried this round
   // static (not dynamic) shared memory: constant-offset LDS addressing
@@ -1483,7 +1486,7 @@ k_mark(Graph g, Sym y) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t b0 = (uint64_t)blockIdx.x * blockDim.x; b0 < g.slots; b0 += stride) {
     const uint64_t p = b0 + threadIdx.x;
-    bool rm = false;
+    bool rm = false;  // queued for k_delta: removed with triangles to carry
     uint32_t id = 0;
     const uint32_t v = p < g.slots ? g.col[p] : 0u;
     if (v != 0) {
@@ -1497,10 +1500,13 @@ k_mark(Graph g, Sym y) {
       const uint32_t sv = u < h0 ? 0u : S[p];  // rows below h0 go whatever their count
       sum_s += sv;
       if (sv < thr || u < h0) {
-        rm = true;
+        ++removed;
         id = g.payload[p];
         const uint32_t c = mark_removed<true>(g, y, (uint32_t)p, u, v, id);
-        if (u < h0 || sv != 0) dcost += c;  // S = 0 (exact above h0): no triangle to carry
+        // S = 0 (exact above h0): the edge closes no triangle, nothing to
+        // carry -- it is neither costed nor queued for k_delta
+        rm = u < h0 || sv != 0;
+        if (rm) dcost += c;
         if (!y.rdirty[u]) y.rdirty[u] = 1;
         if (!y.sdirty[u]) y.sdirty[u] = 1;
       } else {
@@ -1519,7 +1525,6 @@ k_mark(Graph g, Sym y) {
         t += c;
       }
       qbase = t ? atomicAdd(&g.st->nfq[fpar], t) : 0u;
-      removed += t;
     }
     __syncthreads();
     if (rm) fq[qbase + wcnt[wid] + __popc(m & ((1u << lane) - 1u))] = id;
@@ -1530,13 +1535,14 @@ k_mark(Graph g, Sym y) {
     sum_s += __shfl_xor_sync(0xffffffffu, sum_s, o);
     dcost += __shfl_xor_sync(0xffffffffu, dcost, o);
     kcost += __shfl_xor_sync(0xffffffffu, kcost, o);
+    removed += __shfl_xor_sync(0xffffffffu, removed, o);
   }
   if (lane == 0) {
     if (sum_s) atomicAdd(&g.st->sum_s, sum_s);
     if (dcost) atomicAdd(&g.st->delta_cost, dcost);
     if (kcost) atomicAdd(&g.st->keep_cost, kcost);
+    if (removed) atomicAdd(&g.st->removed, removed);
   }
-  if (threadIdx.x == 0 && removed) atomicAdd(&g.st->removed, removed);
 }
 
 // Mode 1: thread per frontier edge (queued by the previous round's k_delta).
@@ -1889,9 +1895,81 @@ k_xapply(Graph g, Sym y, XGroup x) {
 // Oriented rows that lost an edge: stable compaction of (col, id) and, when
 // the round carries supports, S; pos_of follows every moved edge. Warp per
 // queued row up to kHeavyRow (HEAVY = 0), CTA per longer row (HEAVY = 1).
+// Stable in-place compaction of one oriented row [base, base + d) by a group
+// of GS lanes: live entries (no dead mark) move down with their id and,
+// when the round carries, their S; pos_of follows; the vacated tail is
+// zeroed. Returns the new length.
+template <int GS>
+__device__ __forceinline__ uint32_t row_compact(const Graph& g, const Sym& y, uint32_t* __restrict__ S, bool carry,
+                                                uint32_t base, uint32_t d, uint32_t gl, unsigned gmask) {
+  uint32_t write = 0;
+  for (uint32_t off = 0; off < d; off += GS) {
+    const uint32_t idx = off + gl;
+    const bool live = idx < d;
+    const uint32_t c = live ? g.col[base + idx] : 0u;
+    const uint32_t sv = (live && carry) ? S[base + idx] : 0u;
+    const uint32_t pv = live ? g.payload[base + idx] : 0u;
+    const bool keep = live && !(c & kDeadMark);
+    uint32_t x = keep;
+#pragma unroll
+    for (int o = 1; o < GS; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(gmask, x, o, GS);
+      if (gl >= (uint32_t)o) x += t;
+    }
+    const uint32_t total = __shfl_sync(gmask, x, GS - 1, GS);
+    if (keep) {
+      const uint32_t pos = write + x - 1;
+      g.col[base + pos] = c;
+      if (carry) S[base + pos] = sv;
+      g.payload[base + pos] = pv;
+      if (pos != idx) y.pos_of[pv] = base + pos;
+    }
+    write += total;
+  }
+  for (uint32_t x = write + gl; x < d; x += GS) {
+    g.col[base + x] = 0;
+    if (carry) S[base + x] = 0;
+  }
+  return write;
+}
+
 template <int HEAVY>
 __global__ void __launch_bounds__(HEAVY ? kSymHeavyThreads : kPruneThreads)
 k_inc_rows(Graph g, Sym y) {
+  if (!HEAVY) {
+    // a warp takes 4 queued rows: rows of <= 32 entries by one 8-lane group
+    // each, longer ones by the whole warp, rows above kHeavyRow by the CTA
+    // kernel (HEAVY = 1)
+    if (g.st->removed == 0) return;
+    const bool carry = g.st->carry;
+    uint32_t* __restrict__ S = cur_S(g);
+    const uint32_t lane = threadIdx.x & 31, grp = lane >> 3, gl = lane & 7;
+    const unsigned gmask = 0xffu << (grp * 8);
+    const uint32_t nq = g.st->nqrow;
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t h0 = warp * 4; h0 < nq; h0 += nwarps * 4) {  // warp-uniform
+      const uint32_t h = h0 + grp;
+      const uint32_t u = h < nq ? y.qrow[h] : 0u;
+      const uint32_t d = h < nq ? g.deg[u] : 0u;
+      if (h < nq && d <= 32) {
+        const uint32_t nd = row_compact<8>(g, y, S, carry, g.row_ptr[u], d, gl, gmask);
+        if (gl == 0) g.deg[u] = nd;
+      } else if (h < nq && d > (uint32_t)kHeavyRow && gl == 0) {
+        g.heavy_rows[atomicAdd(&g.st->nheavy, 1u)] = u;
+      }
+      __syncwarp();
+      unsigned lm = __ballot_sync(0xffffffffu, gl == 0 && h < nq && d > 32 && d <= (uint32_t)kHeavyRow);
+      while (lm) {
+        const int src = __ffs(lm) - 1;
+        lm &= lm - 1;
+        const uint32_t uu = __shfl_sync(0xffffffffu, u, src), dd = __shfl_sync(0xffffffffu, d, src);
+        const uint32_t nd = row_compact<32>(g, y, S, carry, g.row_ptr[uu], dd, lane, 0xffffffffu);
+        if (lane == 0) g.deg[uu] = nd;
+      }
+    }
+    return;
+  }
   constexpr int EPT = HEAVY ? 4 : 1;
   constexpr int BT = HEAVY ? kSymHeavyThreads : kPruneThreads;
   constexpr int NW = BT / 32;
@@ -1982,10 +2060,71 @@ k_inc_rows(Graph g, Sym y) {
   }
 }
 
+// Stable in-place compaction of one symmetric row by a group of GS lanes
+// (GS = 8 or 32, `gl` = lane in the group, `gmask` = the group's lanes):
+// drops entries whose edge is dead, returns the new length.
+template <int GS>
+__device__ __forceinline__ uint32_t sym_compact(const Sym& y, unsigned long long base, uint32_t d, uint32_t gl,
+                                                unsigned gmask) {
+  uint32_t write = 0;
+  for (uint32_t off = 0; off < d; off += GS) {
+    const uint32_t idx = off + gl;
+    const bool live = idx < d;
+    const uint32_t w = live ? y.nbr[base + idx] : 0u;
+    const uint32_t ev = live ? y.eid[base + idx] : 0u;
+    const bool keep = live && !y.dead[ev];
+    uint32_t x = keep;
+#pragma unroll
+    for (int o = 1; o < GS; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(gmask, x, o, GS);
+      if (gl >= (uint32_t)o) x += t;
+    }
+    const uint32_t total = __shfl_sync(gmask, x, GS - 1, GS);
+    if (keep) {
+      y.nbr[base + write + x - 1] = w;
+      y.eid[base + write + x - 1] = ev;
+    }
+    write += total;
+  }
+  return write;
+}
+
 // Symmetric rows that lost an edge drop their dead entries (stable).
+// HEAVY = 0: a warp takes 4 queued rows; rows of <= 32 entries (most of them
+// in degree order) are compacted by one 8-lane group each, longer ones by the
+// whole warp, rows above kHeavyRow go to the CTA kernel (HEAVY = 1).
 template <int HEAVY>
 __global__ void __launch_bounds__(HEAVY ? kSymHeavyThreads : kPruneThreads)
 k_inc_sym(Graph g, Sym y) {
+  if (!HEAVY) {
+    if (g.st->removed == 0) return;
+    const uint32_t lane = threadIdx.x & 31, grp = lane >> 3, gl = lane & 7;
+    const unsigned gmask = 0xffu << (grp * 8);
+    const uint32_t nq = g.st->nqsym;
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t h0 = warp * 4; h0 < nq; h0 += nwarps * 4) {  // warp-uniform
+      const uint32_t h = h0 + grp;
+      const uint32_t v = h < nq ? y.qsym[h] : 0u;
+      const uint32_t d = h < nq ? y.deg[v] : 0u;
+      if (h < nq && d <= 32) {
+        const uint32_t nd = sym_compact<8>(y, y.ptr[v], d, gl, gmask);
+        if (gl == 0) y.deg[v] = nd;
+      } else if (h < nq && d > (uint32_t)kHeavyRow && gl == 0) {
+        y.heavy[atomicAdd(&g.st->nheavy_sym, 1u)] = v;
+      }
+      __syncwarp();
+      unsigned lm = __ballot_sync(0xffffffffu, gl == 0 && h < nq && d > 32 && d <= (uint32_t)kHeavyRow);
+      while (lm) {  // the warp's medium rows, one at a time, all 32 lanes
+        const int src = __ffs(lm) - 1;
+        lm &= lm - 1;
+        const uint32_t vv = __shfl_sync(0xffffffffu, v, src), dd = __shfl_sync(0xffffffffu, d, src);
+        const uint32_t nd = sym_compact<32>(y, y.ptr[vv], dd, lane, 0xffffffffu);
+        if (lane == 0) y.deg[vv] = nd;
+      }
+    }
+    return;
+  }
   constexpr int EPT = HEAVY ? 4 : 1;
   constexpr int BT = HEAVY ? kSymHeavyThreads : kPruneThreads;
   constexpr int NW = BT / 32;

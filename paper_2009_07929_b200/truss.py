@@ -148,7 +148,7 @@ class _Options(ctypes.Structure):
 
 class _RunInfo(ctypes.Structure):
     _fields_ = [("iterations", _u32), ("live_edges", _u64), ("triangles", _u64),
-                ("max_support", _u32), ("device_ms", ctypes.c_double)]
+                ("max_support", _u32), ("device_ms", ctypes.c_double), ("carried", _u32)]
 
 
 class _RoundWork(ctypes.Structure):

@@ -78,3 +78,21 @@ def test_results_survive_later_calls(port):
     r = kt.ktruss(g, 3)  # buffers released above are reused
     e, _ = port.truss_edges(g, 3, threads=4)
     assert np.array_equal(r.edges, e)
+
+
+def test_engine_reports_carried_mode():
+    """ktg_run_info.carried: 1 when the carried-support structures are
+    resident (default), 0 for recompute-only engines (KTG_FLAG_RECOMPUTE,
+    label order; also a load whose structures do not fit in HBM)."""
+    g = kt.rmat(10, 16, seed=3)
+    e = kt.Engine(g)
+    e.reset()
+    e.run(4)
+    assert e.info()["carried"] == 1
+    e.close()
+    for o in (kt.TrussOptions(recompute=True), kt.TrussOptions(label_order=True)):
+        e = kt.Engine(g, o)
+        e.reset()
+        e.run(4)
+        assert e.info()["carried"] == 0
+        e.close()
