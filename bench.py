@@ -417,14 +417,18 @@ def main():
     hg = kt.ZeroTerminatedCsr(n, keep[0].numpy().view(np.uint32), keep[1].numpy().view(np.uint32))
     e2e_ms, d2h = [], 0
     if world == 1:
-        kt.ktruss(hg, ks[0])  # untimed warm-up: cached host-API engine + pinned result pool
+        for k in ks:  # untimed warm-up: cached host-API engine + pinned result pool
+            kt.ktruss(hg, k)
         for _ in range(max(1, args.e2e_steps)):
             torch.cuda.synchronize()
             t = time.perf_counter()
             d2h = 0
             for k in ks:
+                # a caller keeps the truss it asked for; it drops it before the
+                # next call, so the pooled page-locked buffer is reused
                 r = kt.ktruss(hg, k)
                 d2h += r.nbytes + 8 * r.iterations
+                del r
             e2e_ms.append((time.perf_counter() - t) * 1e3)
         e2e = {"value": len(ks) * m / (min(e2e_ms) / 1e3), "unit": "edges/s",
                "h2d_bytes_per_step": len(ks) * (n + 2 + slots) * 4, "d2h_bytes_per_step": int(d2h),
@@ -458,42 +462,50 @@ def main():
         except Exception:
             peak, peak_src = 6650.0, "fallback"
         ew = kt.Engine(g, kt.TrussOptions(no_degree_bound=True), collect_work=True, time_support=True)
-        tot_b = tot_ms = tot_x = 0.0
-        n_launch = 0
+        # the dominant launch: the first full pass of a fixpoint from pristine
+        # (round 0; the ncu traffic capture is of this launch); later full
+        # passes of the K list are reported as an aggregate alongside
+        first_ms, first_w, rest_b, rest_x, rest_ms, n_rest = [], None, 0.0, 0.0, 0.0, 0
         for k in ks[:4]:
-            best = None
-            for _ in range(2):
+            for rep in range(3):
                 ew.reset()
                 ew.run(k)
                 w = [x for x in ew.round_work() if x["full_pass"]]
-                t = sum(x["support_ms"] for x in w)
-                if best is None or t < best[0]:
-                    best = (t, w)
-            for x in best[1]:
-                tot_b += support_bytes(x, n, slots)
-                tot_x += executed_bytes(x, n, slots, x["live_edges"])
-                tot_ms += x["support_ms"]
-                n_launch += 1
+                first_ms.append(w[0]["support_ms"])
+                first_w = w[0]
+                if rep == 0:
+                    for x in w[1:]:
+                        rest_b += support_bytes(x, n, slots)
+                        rest_x += executed_bytes(x, n, slots, x["live_edges"])
+                        rest_ms += x["support_ms"]
+                        n_rest += 1
         ew.close()
-        achieved = tot_b / (tot_ms / 1e3) / 1e9
+        ms_launch = statistics.median(first_ms)
+        b_launch = support_bytes(first_w, n, slots)
+        x_launch = executed_bytes(first_w, n, slots, first_w["live_edges"])
+        achieved = b_launch / (ms_launch / 1e3) / 1e9
         traffic = None
         try:
             tj = json.load(open(os.path.join(ROOT, "profiles", "support_traffic.json")))
             traffic = tj.get(f"{args.graph}-s{args.scale}-ef{args.ef}")
         except Exception:
             pass
-        ms_launch = tot_ms / max(1, n_launch)
         roof = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": traffic, "peak_source": peak_src,
-                "kernel": "k_support_a22", "launches_measured": n_launch,
-                "bytes_per_launch_avg": tot_b / max(1, n_launch), "ms_per_launch_avg": ms_launch,
-                "executed_bytes_per_launch_avg": tot_x / max(1, n_launch),
-                "executed_frac": round(tot_x / (tot_ms / 1e3) / 1e9 / peak, 4),
+                "kernel": "k_support_a22", "launch": "round-0 full pass from pristine (no degree bound)",
+                "launches_measured": len(first_ms), "bytes_per_launch": b_launch, "ms_per_launch": ms_launch,
+                "executed_bytes_per_launch": x_launch,
+                "executed_frac": round(x_launch / (ms_launch / 1e3) / 1e9 / peak, 4),
                 "dram_frac": (round(traffic / (ms_launch / 1e3) / 1e9 / peak, 4) if traffic else None),
+                "later_full_passes": {"launches": n_rest, "ms": round(rest_ms, 3),
+                                      "frac": round(rest_b / (rest_ms / 1e3) / 1e9 / peak, 4) if rest_ms else None,
+                                      "executed_frac": round(rest_x / (rest_ms / 1e3) / 1e9 / peak, 4)
+                                      if rest_ms else None},
                 "note": "frac = SURVEY §8(d) algorithmic bytes (full merge view: 4 B per element of both "
                         "lists, L) / CUDA-event kernel time -- an effective bandwidth; executed_frac counts "
                         "the bytes the kernel issues (a12 tails + staged A22 chunks + pivots + atomics); "
-                        "dram_frac uses ncu dram__bytes (traffic) of the same kernel"}
+                        "dram_frac = ncu dram__bytes_read+write of this launch (traffic) / its time: the "
+                        "honest HBM fraction"}
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
