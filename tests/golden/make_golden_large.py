@@ -84,8 +84,8 @@ def fast_equal(R, name, g):
 def plan(d):
     jobs = [("s24", k) for k in (936, 935, 3)] + [("er22", 3), ("er22", 4)]
     jobs += [("cl22", "kmax"), ("cl22", "kmax+1")]
-    jobs += [("s24", k) for k in (10, 30, 100, 300)]
     jobs += [("s20", k) for k in range(3, 306)]
+    jobs += [("s24", k) for k in (10, 30, 100, 300)]
     return jobs
 
 

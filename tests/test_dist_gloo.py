@@ -138,3 +138,80 @@ def test_task_split_is_work_balanced():
         assert tot.max() / tot.mean() < 1.02, w
         eq = np.bincount(np.minimum(w - 1, np.arange(Q) * w // Q), weights=c, minlength=w)
         assert eq.max() / eq.mean() > 1.2, w
+
+
+def owner_of(eid, world):
+    """Mirror of ktg_kernels.cuh owner_of: the rank sharding removed edge
+    `eid` in a carried round of the peer group."""
+    return ((eid * 2654435761) & 0xFFFFFFFF) * world >> 32
+
+
+def _support_all(edges, live):
+    adj = {}
+    for i in np.flatnonzero(live):
+        u, v = edges[i]
+        adj.setdefault(u, set()).add(v)
+        adj.setdefault(v, set()).add(u)
+    S = np.zeros(len(edges), np.int64)
+    for i in np.flatnonzero(live):
+        u, v = edges[i]
+        S[i] = len(adj[u] & adj[v])
+    return S, adj
+
+
+def _sharded_carried_fixpoint(rank, world):
+    """The peer group's carried rounds on CPU ranks: each rank finds the lost
+    triangles of its share of the removed edges (owner_of), a triangle is
+    handled by its removed edge of smallest id, the decrement lists are
+    all-gathered and every rank applies all of them. Every round's supports
+    must equal a from-scratch recount, and the fixpoint the reference loop's
+    (truss.cpp:41-53: reset + recount + prune every round)."""
+    import oracle
+    from paper_2009_07929_b200 import graph
+    g = graph.rmat(9, 16, seed=5)
+    rp, col = g.row_ptr.astype(np.int64), g.col_idx
+    rows = np.repeat(np.arange(g.num_vertices + 1), np.diff(rp[:g.num_vertices + 2]))
+    sl = np.flatnonzero(col != 0)
+    edges = np.stack([rows[sl], col[sl].astype(np.int64)], axis=1)
+    eid = {(int(u), int(v)): i for i, (u, v) in enumerate(edges)}
+    out = {}
+    for k in (4, 6, 9):
+        thr = k - 2
+        live = np.ones(len(edges), bool)
+        S, adj = _support_all(edges, live)
+        hist = []
+        while True:
+            rem = live & (S < thr)
+            hist.append(int(rem.sum()))
+            if not rem.any():
+                break
+            dec = []
+            for e in np.flatnonzero(rem):
+                if owner_of(int(e), world) != rank:
+                    continue
+                u, v = edges[e]
+                for w in adj[u] & adj[v]:
+                    a = eid[(min(u, w), max(u, w))]
+                    b = eid[(min(v, w), max(v, w))]
+                    if (rem[a] and a < e) or (rem[b] and b < e):
+                        continue  # a smaller removed id handles this triangle
+                    dec += [x for x in (a, b) if not rem[x]]
+            lists = [None] * world
+            dist.all_gather_object(lists, dec)
+            live &= ~rem
+            for lst in lists:
+                for x in lst:
+                    S[x] -= 1
+            S[~live] = 0
+            fresh, adj = _support_all(edges, live)
+            assert np.array_equal(S, fresh), (k, len(hist))
+        col_e, S_e, hist_e = oracle.port().run_fixpoint(g, k, threads=1)
+        assert hist == hist_e, (k, hist, hist_e)
+        assert int(live.sum()) == int(np.count_nonzero(col_e))
+        out[k] = (hist, int(live.sum()))
+    return out
+
+
+def test_sharded_carried_rounds_match_recount():
+    res = _spawn(_sharded_carried_fixpoint)
+    assert res[0] == res[1]

@@ -156,7 +156,9 @@ def test_carried_run_partitioned_virtual_ranks(port):
     two engines in two threads on one device, byte-exact against the oracle."""
     world = 2
     g = kt.rmat(13, 16, seed=4)
-    engines = [kt.Engine(g) for _ in range(world)]
+    # collect_work: per-round records prove the carried path ran (rounds with
+    # full_pass == 0), not a silent fallback to recompute mode
+    engines = [kt.Engine(g, collect_work=True) for _ in range(world)]
     bar = threading.Barrier(world, timeout=120)
     parts = [None] * world
     slots = g.total_slots()
@@ -190,7 +192,7 @@ def test_carried_run_partitioned_virtual_ranks(port):
                 engines[r].reset()
                 hist = engines[r].run(k)
                 col, S = engines[r].read()
-                out[r][k] = (hist, col.copy(), S.copy())
+                out[r][k] = (hist, col.copy(), S.copy(), engines[r].round_work())
         except Exception as ex:  # pragma: no cover
             errs.append(ex)
             bar.abort()
@@ -205,8 +207,11 @@ def test_carried_run_partitioned_virtual_ranks(port):
     if errs:
         raise errs[0]
     assert slots > 0
+    carried = 0
     for k in ks:
         col_e, S_e, hist_e = port.run_fixpoint(g, k, threads=8)
         for r in range(world):
-            hist, col, S = out[r][k]
+            hist, col, S, work = out[r][k]
             assert hist == hist_e and np.array_equal(col, col_e) and np.array_equal(S, S_e), (r, k)
+            carried += sum(1 for w in work if not w["full_pass"])
+    assert carried > 0, "no carried round ran: the partitioned carried path was not exercised"
