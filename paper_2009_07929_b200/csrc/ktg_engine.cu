@@ -225,6 +225,7 @@ struct ktg_engine {
   uint64_t xcap = 0, xspan = 0;
 
   cudaEvent_t ev0 = nullptr, ev1 = nullptr, evs0 = nullptr, evs1 = nullptr;
+  bool ran = false;  // a fixpoint has recorded ev0 / ev1
   ktg_run_info info{};
   std::vector<ktg_round_work> work;
 
@@ -563,6 +564,7 @@ ktg_status build_working(ktg_engine* e, bool with_sym) {
   tmp = e->cub_tmp.cap;
   KTG_CUDA(cub::DeviceScan::ExclusiveSum(e->cub_tmp.p, tmp, e->sizes.p, W.row_ptr.p, (int)nb, s));
   KTG_CUDA(cudaMemsetAsync(W.col.p, 0, W.slots * 4, s));
+  KTG_CUDA(cudaMemsetAsync(W.id.p, 0, W.slots * 4, s));  // sentinel slots carry id 0 (initcheck-clean copies)
   if (!with_sym) {
     k_fill_working<<<8 * e->num_sms, 256, 0, s>>>(e->keys_sorted.p, e->vals_sorted.p, m, B, W.col.p, W.id.p);
     KTG_CUDA(cudaGetLastError());
@@ -1166,6 +1168,7 @@ ktg_status run_loop(ktg_engine* e, bool want_sync) {
       flag(e, KTG_FLAG_HOST_LOOP) || e->opt.observer || (e->world > 1 && !e->group) || e->nccl || recording;
   e->work.clear();
   e->caller_stale = true;
+  e->ran = true;  // ev0 / ev1 bracket a run from here on
   KTG_CUDA(cudaEventRecord(e->ev0, e->stream));
   if (!host_loop) {
     KTG_TRY(build_graph(e));
@@ -1235,7 +1238,7 @@ ktg_status overflow_error(ktg_engine* e) {
 
 ktg_status finish_info(ktg_engine* e) {
   float ms = 0;
-  if (cudaEventElapsedTime(&ms, e->ev0, e->ev1) != cudaSuccess) {  // no run recorded yet
+  if (e->ran && cudaEventElapsedTime(&ms, e->ev0, e->ev1) != cudaSuccess) {
     cudaGetLastError();
     ms = 0;
   }

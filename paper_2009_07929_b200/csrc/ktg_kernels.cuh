@@ -1948,6 +1948,18 @@ k_inc_rows(Graph g, Sym y) {
     const uint32_t nq = g.st->nqrow;
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    if (nq <= nwarps) {  // few rows (late carried rounds): one warp each, all in parallel
+      for (uint32_t h = warp; h < nq; h += nwarps) {
+        const uint32_t u = y.qrow[h], d = g.deg[u];
+        if (d > (uint32_t)kHeavyRow) {
+          if (lane == 0) g.heavy_rows[atomicAdd(&g.st->nheavy, 1u)] = u;
+          continue;
+        }
+        const uint32_t nd = row_compact<32>(g, y, S, carry, g.row_ptr[u], d, lane, 0xffffffffu);
+        if (lane == 0) g.deg[u] = nd;
+      }
+      return;
+    }
     for (uint32_t h0 = warp * 4; h0 < nq; h0 += nwarps * 4) {  // warp-uniform
       const uint32_t h = h0 + grp;
       const uint32_t u = h < nq ? y.qrow[h] : 0u;
@@ -2103,6 +2115,18 @@ k_inc_sym(Graph g, Sym y) {
     const uint32_t nq = g.st->nqsym;
     const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    if (nq <= nwarps) {  // few rows (late carried rounds): one warp each, all in parallel
+      for (uint32_t h = warp; h < nq; h += nwarps) {
+        const uint32_t v = y.qsym[h], d = y.deg[v];
+        if (d > (uint32_t)kHeavyRow) {
+          if (lane == 0) y.heavy[atomicAdd(&g.st->nheavy_sym, 1u)] = v;
+          continue;
+        }
+        const uint32_t nd = sym_compact<32>(y, y.ptr[v], d, lane, 0xffffffffu);
+        if (lane == 0) y.deg[v] = nd;
+      }
+      return;
+    }
     for (uint32_t h0 = warp * 4; h0 < nq; h0 += nwarps * 4) {  // warp-uniform
       const uint32_t h = h0 + grp;
       const uint32_t v = h < nq ? y.qsym[h] : 0u;
