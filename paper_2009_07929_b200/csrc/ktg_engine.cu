@@ -551,7 +551,12 @@ ktg_status build_working(ktg_engine* e, bool with_sym) {
   // edge keys in caller row order, then sort by (a, b)
   tmp = e->cub_tmp.cap;
   KTG_CUDA(cub::DeviceScan::ExclusiveSum(e->cub_tmp.p, tmp, C.deg.p, e->offs.p, (int)nb, s));
-  if (with_sym) KTG_TRY(sym_alloc(e, m));
+  if (with_sym) {
+    KTG_TRY(sym_alloc(e, m));
+    // pos_of is indexed by caller slot: sentinel slots are never written by
+    // k_fill_all; define them (initcheck-clean pristine copy)
+    KTG_CUDA(cudaMemsetAsync(e->pos_of.p, 0xff, C.slots * 4, s));
+  }
   k_edge_keys<<<e->prune_grid, kPruneThreads, 0, s>>>(g, e->rank.p, e->offs.p, B, e->keys.p, e->vals.p,
                                                       with_sym ? e->erow.p : nullptr);
   KTG_CUDA(cudaGetLastError());

@@ -100,11 +100,15 @@ def engine_join_group(engine: Engine, group: Optional[dist.ProcessGroup] = None)
     return mapped
 
 
+def _reduce_device(device):
+    return device if dist.get_backend() == "nccl" else "cpu"
+
+
 def max_over_ranks(x: float, device: Optional[torch.device] = None) -> float:
     world, _ = world_rank()
     if world == 1:
         return float(x)
-    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=_reduce_device(device))
     dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return float(t.item())
 
@@ -113,7 +117,7 @@ def sum_over_ranks(x: float, device: Optional[torch.device] = None) -> float:
     world, _ = world_rank()
     if world == 1:
         return float(x)
-    t = torch.tensor([float(x)], dtype=torch.float64, device=device)
+    t = torch.tensor([float(x)], dtype=torch.float64, device=_reduce_device(device))
     dist.all_reduce(t, op=dist.ReduceOp.SUM)
     return float(t.item())
 
