@@ -433,6 +433,12 @@ ktg_status read_state(ktg_engine* e) {
 }
 
 __global__ void k_set_live(DevState* st, unsigned long long live) { st->live = live; }
+__global__ void k_reset_state(DevState* st) {
+  const unsigned int ep = st->xepoch;
+  DevState z{};
+  *st = z;
+  st->xepoch = ep;
+}
 __global__ void k_set_rqcap(DevState* st, unsigned long long cap) { st->rq_cap = cap; }
 __global__ void k_clear_heavy(DevState* st) { st->nheavy = 0; }
 
@@ -453,7 +459,9 @@ ktg_status prepare_layout(ktg_engine* e, Layout& L, bool keep_pristine, const ui
   KTG_CUDA(cudaMemsetAsync(L.col.p + L.slots, 0, 16, e->stream));
   KTG_CUDA(cudaMemsetAsync(L.S0.p, 0, sb * 4, e->stream));
   KTG_CUDA(cudaMemsetAsync(L.S1.p, 0, sb * 4, e->stream));
-  KTG_CUDA(cudaMemsetAsync(e->d_st, 0, sizeof(DevState), e->stream));
+  // fresh loop state; the peer-group barrier epoch survives (the peers'
+  // flags in this engine's exchange area hold epochs of earlier barriers)
+  k_reset_state<<<1, 1, 0, e->stream>>>(e->d_st);
   if (known_deg) {  // the builder counted every row (working layout: out-degrees)
     KTG_CUDA(cudaMemcpyAsync(L.deg.p, known_deg, nb * 4, cudaMemcpyDeviceToDevice, e->stream));
     k_set_live<<<1, 1, 0, e->stream>>>(e->d_st, known_live);

@@ -19,7 +19,7 @@ pytestmark = pytest.mark.gpu
 OUT = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
 
 
-def _group_ranks(g, world, ks, opts=None, **kw):
+def _group_ranks(g, world, ks, opts=None, reload=False, **kw):
     engines = [kt.Engine(g, opts, **kw) for _ in range(world)]
     areas = [e.group_area()[0] for e in engines]
     bufs = [e.support_buffers() for e in engines]
@@ -35,6 +35,8 @@ def _group_ranks(g, world, ks, opts=None, **kw):
         try:
             for k in ks:
                 bar.wait()  # every rank runs the same fixpoint sequence
+                if reload:  # same graph again: the group survives the load
+                    engines[r].load(g)
                 engines[r].reset()
                 hist = engines[r].run(k)
                 info = engines[r].info()
@@ -90,6 +92,16 @@ def test_group_virtual_ranks_device_resident(port, world):
     os.makedirs(OUT, exist_ok=True)
     with open(os.path.join(OUT, f"group_overhead_w{world}.json"), "w") as f:
         json.dump(rec, f, indent=1)
+
+
+def test_group_survives_reload(port):
+    """Reloading the same graph keeps the group (same buffers) and the
+    barrier epochs (the loop state is reset, the peers' flags are not): a
+    multi-rank end-to-end run reloads before every fixpoint."""
+    g = kt.rmat(12, 16, seed=9)
+    ks = (3, 5, 8)
+    out = _group_ranks(g, 2, ks, reload=True)
+    _check(port, g, out, ks)
 
 
 def test_group_carried_rounds_are_sharded(port):
