@@ -839,9 +839,6 @@ k_support_chunked(Graph g) {
 #define KTG_A22_UNROLL 4
 #endif
 constexpr int kA22Batch = 256;
-#ifndef KTG_A22_CONSEC
-#define KTG_A22_CONSEC 0   // consecutive elements per lane (A/B)
-#endif
 #ifndef KTG_A22_LIGHT
 #define KTG_A22_LIGHT 1    // round-0 light pivots skip their increments
 #endif
@@ -1095,43 +1092,6 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ wcost) {
           prun = s.prun[p];
         }
       };
-#if KTG_A22_CONSEC
-      // lane l takes kA22Unroll CONSECUTIVE elements per step: its pivot
-      // changes at most about once per step (tails average ~12 elements), so
-      // the per-element pivot advance of the strided mapping becomes one
-      // binary search per lane per step over the <= 32*U pivots from p0 (the
-      // pivot holding the step's first element)
-      for (uint32_t f0 = base; f0 < lim; f0 += 32 * kA22Unroll) {  // warp-uniform trips
-        const uint32_t f = f0 + kA22Unroll * lane;
-        if (f < lim) {
-          uint32_t lo = p, len = min((uint32_t)kA22Batch - p, 32u * kA22Unroll);
-          while (len > 0) {  // last q in [lo, lo + len] with pref[q] <= f
-            const uint32_t half = (len + 1) >> 1;
-            if (s.pref[lo + half] <= f) {
-              lo += half;
-              len -= half;
-            } else {
-              len = half - 1;
-            }
-          }
-          p = lo;
-          pe_ = s.pref[p + 1], pb = s.pref[p], plo = s.plo[p], prun = s.prun[p];
-        }
-        uint32_t sl[kA22Unroll], ru[kA22Unroll], pv[kA22Unroll], cv[kA22Unroll];
-#pragma unroll
-        for (int u = 0; u < kA22Unroll; ++u) {
-          const uint32_t fu = f + u;
-          if (fu < lim) advance(fu);
-          sl[u] = plo + (fu - pb), ru[u] = prun, pv[u] = p;
-        }
-#pragma unroll
-        for (int u = 0; u < kA22Unroll; ++u) cv[u] = (f + u < lim) ? col[sl[u]] : 0u;
-#pragma unroll
-        for (int u = 0; u < kA22Unroll; ++u)
-          if (f + u < lim) probe(cv[u], sl[u], ru[u], pv[u]);
-        p = __shfl_sync(0xffffffffu, p, 31);  // the pivot of the step's last element
-      }
-#else
       // kA22Unroll elements per lane per step, every load issued before any probe
       for (uint32_t f = base + lane; f < lim; f += 32 * kA22Unroll) {
         uint32_t sl[kA22Unroll], ru[kA22Unroll], pv[kA22Unroll], cv[kA22Unroll];
@@ -1147,7 +1107,6 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ wcost) {
         for (int u = 0; u < kA22Unroll; ++u)
           if (f + 32 * u < lim) probe(cv[u], sl[u], ru[u], pv[u]);
       }
-#endif
     }
     tri_local += tri_task;
     __syncthreads();
