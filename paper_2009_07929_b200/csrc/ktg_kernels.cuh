@@ -839,18 +839,6 @@ k_support_chunked(Graph g) {
 #define KTG_A22_UNROLL 4
 #endif
 constexpr int kA22Batch = 256;
-#ifndef KTG_A22_REDHINT
-#define KTG_A22_REDHINT 0  // S reds with an L2 evict_first policy (A/B)
-#endif
-#ifndef KTG_A22_LDHINT
-#define KTG_A22_LDHINT 0   // tail loads with an L2 evict_last policy (A/B)
-#endif
-#ifndef KTG_A22_LDG
-#define KTG_A22_LDG 0      // tail loads through the read-only path (A/B)
-#endif
-#ifndef KTG_A22_PREFETCH
-#define KTG_A22_PREFETCH 0  // L2 prefetch of the strip's tail starts (A/B)
-#endif
 #ifndef KTG_A22_LIGHT
 #define KTG_A22_LIGHT 1    // round-0 light pivots skip their increments
 #endif
@@ -915,13 +903,6 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ wcost) {
   const uint32_t h0 = g.st->h0;
   const bool pristine = g.st->pristine;
   unsigned long long tri_local = 0;
-#if KTG_A22_REDHINT
-  uint64_t l2pol;  // S updates leave L2 first: keep the re-read tail rows
-  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(l2pol));
-#elif KTG_A22_LDHINT
-  uint64_t l2pol;  // tail rows stay in L2 longer than the S updates
-  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(l2pol));
-#endif
 
   for (;;) {
     if (tid == 0) {
@@ -1074,14 +1055,6 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ wcost) {
         p = 8 * g + c2;
       }
       uint32_t pe_ = s.pref[p + 1], pb = s.pref[p], plo = s.plo[p], prun = s.prun[p];
-#if KTG_A22_PREFETCH
-      {  // the strip's pivots (one per lane): pull the start of each tail
-         // towards L2 before the lanes reach it
-        const uint32_t q = p + lane;
-        if (q < (uint32_t)kA22Batch && s.pref[q] < lim && s.pref[q + 1] > s.pref[q])
-          asm volatile("prefetch.global.L2 [%0];" ::"l"(col + s.plo[q]));
-      }
-#endif
       // (value, run) lookup of tail element c of pivot pp: the value may also
       // sit in other rows' runs
       auto probe = [&](uint32_t c, uint32_t slot, uint32_t run, uint32_t pp) {
@@ -1101,11 +1074,7 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ wcost) {
           if (x < (uint32_t)kChunk) {
             atomicAdd(&s.cntA[x], 1u);
             if (!KTG_A22_LIGHT || !(run >> 31)) {
-#if KTG_A22_REDHINT
-              asm volatile("red.global.add.L2::cache_hint.u32 [%0], 1, %1;" ::"l"(S + slot), "l"(l2pol) : "memory");
-#else
               atomicAdd(&S[slot], 1u);
-#endif
               atomicAdd(&s.cntP[pp], 1u);
             }
             ++tri_task;
@@ -1133,18 +1102,7 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ wcost) {
           sl[u] = plo + (fu - pb), ru[u] = prun, pv[u] = p;
         }
 #pragma unroll
-        for (int u = 0; u < kA22Unroll; ++u) {
-#if KTG_A22_LDHINT
-          uint32_t vv = 0u;
-          if (f + 32 * u < lim)
-            asm volatile("ld.global.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(vv) : "l"(col + sl[u]), "l"(l2pol));
-          cv[u] = vv;
-#elif KTG_A22_LDG
-          cv[u] = (f + 32 * u < lim) ? __ldg(col + sl[u]) : 0u;
-#else
-          cv[u] = (f + 32 * u < lim) ? col[sl[u]] : 0u;
-#endif
-        }
+        for (int u = 0; u < kA22Unroll; ++u) cv[u] = (f + 32 * u < lim) ? col[sl[u]] : 0u;
 #pragma unroll
         for (int u = 0; u < kA22Unroll; ++u)
           if (f + 32 * u < lim) probe(cv[u], sl[u], ru[u], pv[u]);
