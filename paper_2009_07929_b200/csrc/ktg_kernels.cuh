@@ -842,9 +842,15 @@ constexpr int kA22Batch = 256;
 #ifndef KTG_A22_LIGHT
 #define KTG_A22_LIGHT 1    // round-0 light pivots skip their increments
 #endif
+#ifndef KTG_A22_TABLE
+#define KTG_A22_TABLE 2048
+#endif
+#ifndef KTG_A22_UNION
+#define KTG_A22_UNION 1
+#endif
 constexpr int kA22TableBits = 11;          // 2048 slots for <= 512 entries (load <= 0.25)
 constexpr int kA22Strip = 256;             // flat tail elements a warp takes per grab
-constexpr int kA22Table = 1 << kA22TableBits;
+constexpr int kA22Table = KTG_A22_TABLE;     // slots (a power of two uses the top hash bits)
 constexpr int kA22Unroll = KTG_A22_UNROLL;     // tail elements per lane per step (loads in flight)
 constexpr int kA22FiltWords = 512;         // 16K filter bits for <= 512 entries (~3% false positives)
 
@@ -858,16 +864,33 @@ struct A22 {
 };
 
 struct A22Smem {
+#if KTG_A22_UNION
+  // steps 1-2 only (rte, roff) alias step 3+ only (A, filt): dead before the
+  // staging starts, so the CTA stays under the shared-memory size that leaves
+  // the most L1 for the re-read tails at 6 CTAs per SM
+  union {
+    uint32_t rte[kChunk + 2];        // per row of the chunk: run [tb, te) as tb << 16 | te, or ~0
+    uint32_t A[kChunk];
+  };
+  union {
+    uint32_t roff[kChunk + 2];       // pin_off of the chunk's rows (+1)
+    uint32_t filt[kA22FiltWords];    // membership bits of (value, run end): most misses stop here
+  };
+  uint32_t cntA[kChunk];
+#else
   uint32_t A[kChunk];
   uint32_t cntA[kChunk];
   uint32_t rte[kChunk + 2];          // per row of the chunk: run [tb, te) as tb << 16 | te, or ~0
   uint32_t roff[kChunk + 2];         // pin_off of the chunk's rows (+1)
+#endif
   uint32_t ps[kA22Batch];            // pivot slot (i, j)
   uint32_t plo[kA22Batch];           // first tail slot probed
   uint32_t prun[kA22Batch];          // j's run tb << 16 | te
   uint32_t cntP[kA22Batch];
   uint32_t pref[kA22Batch + 1];
+#if !KTG_A22_UNION
   uint32_t filt[kA22FiltWords];      // membership bits of (value, run end): most misses stop here
+#endif
   uint2 tab[kA22Table];              // open addressing: {value (0 = empty), chunk position}
   uint32_t red[kSupportThreads / 32];
   uint32_t task;
@@ -879,7 +902,14 @@ struct A22Smem {
 __device__ __forceinline__ uint32_t a22_mix(uint32_t v, uint32_t te) {
   return (v ^ (te * 0x85EBCA6Bu)) * 2654435761u;
 }
-__device__ __forceinline__ uint32_t a22_slot(uint32_t h) { return h >> (32 - kA22TableBits); }
+__device__ __forceinline__ uint32_t a22_slot(uint32_t h) {
+  if ((kA22Table & (kA22Table - 1)) == 0) return h >> (32 - kA22TableBits);
+  return (uint32_t)(((uint64_t)h * kA22Table) >> 32);  // range reduction for other sizes
+}
+__device__ __forceinline__ uint32_t a22_next(uint32_t h) {
+  if ((kA22Table & (kA22Table - 1)) == 0) return (h + 1) & (kA22Table - 1);
+  return h + 1 == (uint32_t)kA22Table ? 0u : h + 1;
+}
 __device__ __forceinline__ uint32_t a22_fbit(uint32_t h) { return (h ^ (h >> 15)) & (kA22FiltWords * 32 - 1); }
 
 // COST = true (multi-rank runs, before every full pass): steps 1-2 only, over
@@ -1030,7 +1060,7 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ wcost) {
           const uint32_t fb = a22_fbit(hh);
           atomicOr(&s.filt[fb >> 5], 1u << (fb & 31));
           uint32_t h = a22_slot(hh);
-          while (atomicCAS(&s.tab[h].x, 0u, v) != 0u) h = (h + 1) & (kA22Table - 1);
+          while (atomicCAS(&s.tab[h].x, 0u, v) != 0u) h = a22_next(h);
           s.tab[h].y = x;
         }
       }
@@ -1063,7 +1093,7 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ wcost) {
         const uint32_t fb = a22_fbit(hh);
         if (s.filt[fb >> 5] & (1u << (fb & 31))) {
           uint32_t x = kChunk;
-          for (uint32_t h = a22_slot(hh);; h = (h + 1) & (kA22Table - 1)) {
+          for (uint32_t h = a22_slot(hh);; h = a22_next(h)) {
             const uint2 e = s.tab[h];
             if (e.x == 0) break;
             if (e.x == c && e.y - tb < te - tb) {
