@@ -843,12 +843,16 @@ constexpr int kA22Batch = 256;
 #define KTG_A22_LIGHT 1    // round-0 light pivots skip their increments
 #endif
 #ifndef KTG_A22_TABLE
-#define KTG_A22_TABLE 2048
+// 1,920 slots (load <= 0.27): with the aliased step-1/2 arrays the CTA needs
+// 26.7 KB, so 6 CTAs fit the 164 KB shared-memory carveout and L1 keeps 92 KB
+// for the re-read tail rows (2,048 slots cross into the 196 KB carveout:
+// 163 vs 155 ms per s24 pass; 1,216 with the 132 KB carveout: 163 ms)
+#define KTG_A22_TABLE 1920
 #endif
 #ifndef KTG_A22_UNION
 #define KTG_A22_UNION 1
 #endif
-constexpr int kA22TableBits = 11;          // 2048 slots for <= 512 entries (load <= 0.25)
+constexpr int kA22TableBits = 11;          // top hash bits when the table size is a power of two
 constexpr int kA22Strip = 256;             // flat tail elements a warp takes per grab
 constexpr int kA22Table = KTG_A22_TABLE;     // slots (a power of two uses the top hash bits)
 constexpr int kA22Unroll = KTG_A22_UNROLL;     // tail elements per lane per step (loads in flight)
