@@ -2265,11 +2265,77 @@ k_inc_sym(Graph g, Sym y) {
 // pristine row (the composition of every round's prune, truss.cpp:26-35) and
 // take their support from the working slot pos_of[s]. Warp per row up to
 // kHeavyRow (HEAVY = 0, longer rows queued), CTA per longer row (HEAVY = 1).
+// One caller row by a group of GS lanes (GS = 8 or 32): survivors of the
+// pristine row [base, base + d) compacted stably with their supports, the
+// rest zeroed; returns the new length.
+template <int GS>
+__device__ __forceinline__ uint32_t publish_row(const Graph& c, const uint32_t* __restrict__ col_p,
+                                                const uint8_t* __restrict__ dead,
+                                                const uint32_t* __restrict__ pos_of,
+                                                const uint32_t* __restrict__ Sw, uint32_t base, uint32_t d,
+                                                uint32_t gl, unsigned gmask) {
+  uint32_t write = 0;
+  for (uint32_t off = 0; off < d; off += GS) {
+    const uint32_t idx = off + gl;
+    const bool keep = idx < d && !dead[base + idx];
+    const uint32_t cv = keep ? col_p[base + idx] : 0u;
+    const uint32_t sv = keep ? Sw[pos_of[base + idx]] : 0u;
+    uint32_t x = keep;
+#pragma unroll
+    for (int o = 1; o < GS; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(gmask, x, o, GS);
+      if (gl >= (uint32_t)o) x += t;
+    }
+    const uint32_t total = __shfl_sync(gmask, x, GS - 1, GS);
+    if (keep) {
+      c.col[base + write + x - 1] = cv;
+      c.S0[base + write + x - 1] = sv;
+    }
+    write += total;
+  }
+  for (uint32_t x = write + gl; x < d; x += GS) {
+    c.col[base + x] = 0;
+    c.S0[base + x] = 0;
+  }
+  return write;
+}
+
 template <int HEAVY>
 __global__ void __launch_bounds__(HEAVY ? kSymHeavyThreads : kPruneThreads)
 k_publish_inc(Graph c, const uint32_t* __restrict__ col_p, const uint32_t* __restrict__ deg_p,
               const uint8_t* __restrict__ dead, const uint32_t* __restrict__ pos_of,
               const uint32_t* __restrict__ Sw) {
+  if (!HEAVY) {
+    // a warp takes 4 caller rows: rows of <= 32 pristine entries by one 8-lane
+    // group each, longer ones by the whole warp, rows above kHeavyRow by the
+    // CTA kernel (HEAVY = 1)
+    const uint32_t lane = threadIdx.x & 31, grp = lane >> 3, gl = lane & 7;
+    const unsigned gmask = 0xffu << (grp * 8);
+    const uint32_t nq = c.n;
+    const uint32_t warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const uint32_t nwarps = (gridDim.x * blockDim.x) >> 5;
+    for (uint32_t h0 = warp * 4; h0 < nq; h0 += nwarps * 4) {  // warp-uniform
+      const uint32_t h = h0 + grp;
+      const uint32_t r = h + 1;
+      const uint32_t d = h < nq ? deg_p[r] : 0u;
+      if (d != 0 && d <= 32) {
+        const uint32_t nd = publish_row<8>(c, col_p, dead, pos_of, Sw, c.row_ptr[r], d, gl, gmask);
+        if (gl == 0) c.deg[r] = nd;
+      } else if (d > (uint32_t)kHeavyRow && gl == 0) {
+        c.heavy_rows[atomicAdd(&c.st->nheavy, 1u)] = r;
+      }
+      __syncwarp();
+      unsigned lm = __ballot_sync(0xffffffffu, gl == 0 && d > 32 && d <= (uint32_t)kHeavyRow);
+      while (lm) {
+        const int src = __ffs(lm) - 1;
+        lm &= lm - 1;
+        const uint32_t rr = __shfl_sync(0xffffffffu, r, src), dd = __shfl_sync(0xffffffffu, d, src);
+        const uint32_t nd = publish_row<32>(c, col_p, dead, pos_of, Sw, c.row_ptr[rr], dd, lane, 0xffffffffu);
+        if (lane == 0) c.deg[rr] = nd;
+      }
+    }
+    return;
+  }
   constexpr int EPT = HEAVY ? 4 : 1;
   constexpr int BT = HEAVY ? kSymHeavyThreads : kPruneThreads;
   constexpr int NW = BT / 32;
