@@ -93,12 +93,20 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--threads", type=int, default=os.cpu_count())
     ap.add_argument("--only", default=None, help="comma list of graph names")
+    ap.add_argument("--kmin", type=int, default=0, help="only K >= kmin (split a sweep across machines)")
+    ap.add_argument("--kmax", type=int, default=1 << 30, help="only K <= kmax")
+    ap.add_argument("--out", default=None, help="write here instead of tests/golden/large_ref.json")
     args = ap.parse_args()
+    global OUT
+    if args.out:
+        OUT = args.out
     R = oracle.ref()
     d = load()
     graphs = {}
     for name, k in plan(d):
         if args.only and name not in args.only.split(","):
+            continue
+        if isinstance(k, int) and not args.kmin <= k <= args.kmax:
             continue
         ent = d.setdefault(name, {"fixpoints": {}})
         kk = KMAX_CLAIM[name] + (k == "kmax+1") if k in ("kmax", "kmax+1") else k
