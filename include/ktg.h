@@ -256,7 +256,8 @@ ktg_status ktg_engine_extract(ktg_engine* e, uint32_t* out_u, uint32_t* out_v,
 /* Multi-GPU, host-driven exchange: every full support pass
  * covers this rank's share of the support tasks only -- in carried-support
  * runs (the default) a contiguous range of the A22 tasks split by a prefix
- * sum of their exact work on the current graph; in KTG_FLAG_RECOMPUTE runs a
+ * sum of their exact work on the pristine graph, computed once per load; in
+ * KTG_FLAG_RECOMPUTE runs a
  * work-balanced range of chunk tasks -- and the caller all-reduces the
  * support buffer through the allreduce callback on the engine stream. The
  * callback runs after every FULL support pass only (carried rounds are

@@ -181,6 +181,7 @@ struct ktg_engine {
   // multi-rank full passes: per-task work (k_support_a22<true>) and its
   // exclusive prefix (ntasks + 1 entries; cost[ntasks] stays 0)
   DBuf<unsigned long long> a22_cost, a22_pre;
+  uint32_t a22_lo = 0, a22_hi = 0;  // this rank's task range (world > 1)
   bool a22_ready = false;
   bool a22_off_env = false;   // KTG_SUPPORT=chunked: keep k_support_chunked in carried runs
   int a22_grid = 0;
@@ -257,6 +258,8 @@ struct ktg_engine {
     g.npeer = npeer;
     g.xa = (group && world > 1) ? reinterpret_cast<XArea*>(xarea.p) : nullptr;
     g.xcap = xcap;
+    g.a22_lo = a22_lo;
+    g.a22_hi = a22_hi;
     return g;
   }
 
@@ -649,6 +652,41 @@ ktg_status build_a22(ktg_engine* e) {
   return KTG_OK;
 }
 
+__global__ void k_cost_state(DevState* st) {  // a pristine full-pass round for the cost pass
+  st->mode = 0;
+  st->pristine = 1;
+  st->h0 = 0;
+  st->task_next = 0;
+}
+
+// Multi-rank runs: split the A22 tasks across ranks by the exact work of
+// every task on the pristine graph (steps 1-2 of the pass over all tasks,
+// prefix sum, k_a22_split), once per load or partition change. Round 0 of
+// every fixpoint from pristine is the dominant full pass; later full passes
+// reuse the split (balance approximate, results exact either way). The loop
+// state fields touched are reset by k_begin before every run.
+ktg_status a22_rank_split(ktg_engine* e) {
+  e->a22_lo = 0;
+  e->a22_hi = e->a22_ntasks;
+  if (e->world <= 1 || !e->a22_ready || !e->reoriented) return KTG_OK;
+  Layout& W = e->wl;
+  Graph g = e->graph_of(W);
+  const cudaStream_t s = e->stream;
+  A22 a{e->a22_pe.p, e->a22_pin.p, e->a22_off.p, e->a22_jfirst.p, e->a22_tasks.p, e->a22_ntasks};
+  k_cost_state<<<1, 1, 0, s>>>(e->d_st);
+  k_support_a22<true><<<e->a22_grid, kSupportThreads, e->a22_smem, s>>>(g, e->sym(), a, e->a22_cost.p);
+  size_t tmp = e->cub_tmp.cap;
+  KTG_CUDA(cub::DeviceScan::ExclusiveSum(e->cub_tmp.p, tmp, e->a22_cost.p, e->a22_pre.p, (int)e->a22_ntasks + 1, s));
+  k_a22_split<<<1, 1, 0, s>>>(e->d_st, e->a22_pre.p, e->a22_ntasks, e->rank_id, e->world);
+  KTG_CUDA(cudaGetLastError());
+  KTG_TRY(read_state(e));
+  e->a22_lo = e->h_st->a22_lo;
+  e->a22_hi = e->h_st->a22_hi;
+  if (e->exec) cudaGraphExecDestroy(e->exec);  // the range is baked into the graph's kernel arguments
+  e->exec = nullptr;
+  return KTG_OK;
+}
+
 // Buffers of the symmetric adjacency (build_working fills them when it
 // builds with_sym): row v = sorted in-neighbours ++ out-neighbours (working
 // row v), each with the edge id; pos_of / erow per edge id; the A22 in-edge
@@ -790,7 +828,7 @@ ktg_status engine_load(ktg_engine* e, const uint32_t* row_ptr, uint32_t n, const
     e->world = g_world;
     e->rank_id = g_rank;
   }
-  return KTG_OK;
+  return a22_rank_split(e);  // partitioned engines: this graph's task split
 }
 
 const char* kValidateMsg[6] = {"", " owns no sentinel slot", " does not end in a zero slot",
@@ -960,15 +998,6 @@ ktg_status enqueue_round(ktg_engine* e, bool graph_mode, cudaGraphConditionalHan
   if (sup0) KTG_CUDA(cudaEventRecord(sup0, s));
   if (a22) {
     A22 a{e->a22_pe.p, e->a22_pin.p, e->a22_off.p, e->a22_jfirst.p, e->a22_tasks.p, e->a22_ntasks};
-    if (e->world > 1) {
-      // work-balanced split of this full pass across ranks: exact per-task
-      // work on the current graph, prefix sum, this rank's contiguous range
-      k_support_a22<true><<<e->a22_grid, kSupportThreads, e->a22_smem, s>>>(g, e->sym(), a, e->a22_cost.p);
-      size_t tmp = e->cub_tmp.cap;
-      KTG_CUDA(cub::DeviceScan::ExclusiveSum(e->cub_tmp.p, tmp, e->a22_cost.p, e->a22_pre.p,
-                                             (int)e->a22_ntasks + 1, s));
-      k_a22_split<<<1, 1, 0, s>>>(e->d_st, e->a22_pre.p, e->a22_ntasks, e->rank_id, e->world);
-    }
     k_support_a22<false><<<e->a22_grid, kSupportThreads, e->a22_smem, s>>>(g, e->sym(), a, nullptr);
   } else if (flag(e, KTG_FLAG_NAIVE_SUPPORT)) {
     k_support_naive<<<4 * e->num_sms, 256, 0, s>>>(g);
@@ -1694,6 +1723,7 @@ ktg_status ktg_engine_set_partition(ktg_engine* e, uint32_t rank, uint32_t world
   e->world = world;
   e->allreduce = allreduce;
   e->allreduce_user = user;
+  KTG_TRY(a22_rank_split(e));
   if (e->exec) cudaGraphExecDestroy(e->exec);
   e->exec = nullptr;
   return KTG_OK;
@@ -1800,6 +1830,7 @@ ktg_status ktg_engine_set_group(ktg_engine* e, uint32_t rank, uint32_t world, vo
   e->rank_id = rank;
   e->world = world;
   e->group = true;
+  KTG_TRY(a22_rank_split(e));
   // recompute runs plan a work-balanced chunk split every round inside the
   // captured graph: size its buffers now
   const size_t nq = (size_t)L.nchunks + 1;
@@ -1856,7 +1887,7 @@ ktg_status ktg_engine_set_nccl(ktg_engine* e, uint32_t rank, uint32_t world, con
   e->allreduce = nullptr;
   if (e->exec) cudaGraphExecDestroy(e->exec);
   e->exec = nullptr;
-  return KTG_OK;
+  return a22_rank_split(e);
 }
 
 // ---------------------------------------------------------------------------

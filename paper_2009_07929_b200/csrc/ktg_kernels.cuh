@@ -73,7 +73,7 @@ struct DevState {
   double delta_ratio0;               // the same for round 0 of a run from the pristine graph
   unsigned int dq_lo, dq_hi;         // this rank's diagonal support tasks: chunks [dq_lo, dq_hi)
   unsigned long long rq_cap;         // delta piece queue capacity (a round that could exceed it recomputes)
-  unsigned int a22_lo, a22_hi;       // this rank's A22 tasks [lo, hi) of the current full pass (world > 1)
+  unsigned int a22_lo, a22_hi;       // k_a22_split's result (read back into Graph::a22_lo/hi)
   unsigned int xepoch;               // peer group: barriers passed (never reset by a run)
   unsigned int pad4;
 };
@@ -127,6 +127,10 @@ struct Graph {
   // also listed for the peers (k_xapply)
   XArea* xa;
   uint64_t xcap;
+  // multi-rank full passes: this rank's A22 tasks [a22_lo, a22_hi), split by
+  // the pristine graph's exact task work (k_support_a22<true> + k_a22_split,
+  // once per load)
+  uint32_t a22_lo, a22_hi;
 };
 
 // Rank owning removed edge id in a sharded carried round (a hash, so the
@@ -942,8 +946,8 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ wcost) {
     if (tid == 0) {
       // multi-rank runs: this rank's contiguous, work-balanced task range
       const bool part = g.world > 1 && !COST;
-      const uint32_t tt = atomicAdd(&g.st->task_next, 1u) + (part ? g.st->a22_lo : 0u);
-      s.task = tt < (part ? g.st->a22_hi : a.ntasks) ? tt : 0xffffffffu;
+      const uint32_t tt = atomicAdd(&g.st->task_next, 1u) + (part ? g.a22_lo : 0u);
+      s.task = tt < (part ? g.a22_hi : a.ntasks) ? tt : 0xffffffffu;
       s.next = 0;
     }
     __syncthreads();
@@ -1197,13 +1201,13 @@ __global__ void k_a22_fill(const uint32_t* __restrict__ cnt_off, uint32_t nchunk
   for (uint32_t b = 0; b < c; ++b) tasks[o + b] = make_uint2(q, b);
 }
 
-// Multi-rank full pass: rank r takes the contiguous tasks
+// Multi-rank split, computed once per load on the pristine
+// graph (round 0 dominates every fixpoint): rank r takes the contiguous tasks
 // [lo, hi) whose exclusive work prefix pre[t] (over k_support_a22<true>'s
 // costs, pre[ntasks] = total) falls in [total*r/world, total*(r+1)/world);
 // every rank computes the same split from the same replicated state.
 __global__ void k_a22_split(DevState* st, const unsigned long long* __restrict__ pre, uint32_t ntasks,
                             uint32_t rank, uint32_t world) {
-  if (st->mode) return;
   const unsigned long long total = pre[ntasks];
   auto first_at = [&](unsigned long long bound) {  // first t with pre[t] >= bound
     uint32_t lo = 0, hi = ntasks;
