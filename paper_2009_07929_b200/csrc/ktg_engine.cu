@@ -177,6 +177,7 @@ struct ktg_engine {
   // rows, (chunk, batch) tasks
   DBuf<uint32_t> a22_pe, a22_off, a22_jfirst, a22_cnt;
   DBuf<uint2> a22_tasks, a22_pin;
+  DBuf<uint32_t> a22_pin_end;  // pristine pivots: end of the pivot row's live part
   uint32_t a22_ntasks = 0;
   // multi-rank full passes: per-task work (k_support_a22<true>) and its
   // exclusive prefix (ntasks + 1 entries; cost[ntasks] stays 0)
@@ -311,6 +312,7 @@ struct ktg_engine {
     rq.release();
     a22_tasks.release();
     a22_pin.release();
+    a22_pin_end.release();
     a22_cost.release();
     a22_pre.release();
     sym_ready = false;
@@ -349,6 +351,7 @@ struct ktg_engine {
     a22_cost.release();
     a22_pre.release();
     a22_pin.release();
+    a22_pin_end.release();
     sym_ready = false;
     a22_ready = false;
   }
@@ -602,7 +605,8 @@ ktg_status build_working(ktg_engine* e, bool with_sym) {
   KTG_CUDA(cub::DeviceRadixSort::SortPairs(e->cub_tmp.p, tmp, e->vals.p, e->vals_sorted.p, e->keys.p,
                                            e->keys_sorted.p, (int64_t)m, 0, (int)B, s));
   k_fill_in_all<<<8 * e->num_sms, 256, 0, s>>>(e->vals_sorted.p, e->keys_sorted.p, m, sz + 3 * nb, W.id.p, y,
-                                               e->a22_pe.p, e->a22_pin.p);
+                                               e->a22_pe.p, e->a22_pin.p, e->a22_pin_end.p, W.row_ptr.p,
+                                               e->cntw.p);
   KTG_CUDA(cudaGetLastError());
   KTG_CUDA(cudaMemcpyAsync(e->sym_deg.p, e->symdeg_w.p, nb * 4, cudaMemcpyDeviceToDevice, s));
   return prepare_layout(e, W, true, e->cntw.p, m);
@@ -672,7 +676,7 @@ ktg_status a22_rank_split(ktg_engine* e) {
   Layout& W = e->wl;
   Graph g = e->graph_of(W);
   const cudaStream_t s = e->stream;
-  A22 a{e->a22_pe.p, e->a22_pin.p, e->a22_off.p, e->a22_jfirst.p, e->a22_tasks.p, e->a22_ntasks};
+  A22 a{e->a22_pe.p, e->a22_pin.p, e->a22_pin_end.p, e->a22_off.p, e->a22_jfirst.p, e->a22_tasks.p, e->a22_ntasks};
   k_cost_state<<<1, 1, 0, s>>>(e->d_st);
   k_support_a22<true><<<e->a22_grid, kSupportThreads, e->a22_smem, s>>>(g, e->sym(), a, e->a22_cost.p);
   size_t tmp = e->cub_tmp.cap;
@@ -716,6 +720,7 @@ ktg_status sym_alloc(ktg_engine* e, uint64_t m) {
   KTG_TRY(e->dead.ensure(e->cl.slots));
   KTG_TRY(e->a22_pe.ensure(m));
   KTG_TRY(e->a22_pin.ensure(m));
+  KTG_TRY(e->a22_pin_end.ensure(m));
   return KTG_OK;
 }
 
@@ -997,7 +1002,7 @@ ktg_status enqueue_round(ktg_engine* e, bool graph_mode, cudaGraphConditionalHan
   }
   if (sup0) KTG_CUDA(cudaEventRecord(sup0, s));
   if (a22) {
-    A22 a{e->a22_pe.p, e->a22_pin.p, e->a22_off.p, e->a22_jfirst.p, e->a22_tasks.p, e->a22_ntasks};
+    A22 a{e->a22_pe.p, e->a22_pin.p, e->a22_pin_end.p, e->a22_off.p, e->a22_jfirst.p, e->a22_tasks.p, e->a22_ntasks};
     k_support_a22<false><<<e->a22_grid, kSupportThreads, e->a22_smem, s>>>(g, e->sym(), a, nullptr);
   } else if (flag(e, KTG_FLAG_NAIVE_SUPPORT)) {
     k_support_naive<<<4 * e->num_sms, 256, 0, s>>>(g);

@@ -865,6 +865,7 @@ constexpr int kA22FiltWords = 512;         // 16K filter bits for <= 512 entries
 struct A22 {
   const uint32_t* pe;        // in-edge ids, grouped by j (pristine in-lists)
   const uint2* pin_p;        // the same pivots in the pristine graph: {slot, row i}
+  const uint32_t* pin_end;   // ... and the end of row i's live part (its tail end)
   const uint32_t* pin_off;   // n+2: start of j's in-list in pe
   const uint32_t* jfirst;    // per chunk: row holding the chunk's first slot
   const uint2* tasks;        // (chunk, batch)
@@ -969,7 +970,11 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ wcost) {
       if (r < nrows) {
         const uint64_t rb = g.row_ptr[j], re = rb + g.deg[j];
         const uint64_t lo = rb > a0 ? rb : a0, hi = re < a0 + alen ? re : a0 + alen;
-        s.rte[r] = (lo < hi && j >= h0 && j != 0) ? (uint32_t)((lo - a0) << 16 | (hi - a0)) : 0xffffffffu;
+        // tb << 16 | te, bit 30: j's row continues outside the chunk (its
+        // pivots' tails get clipped to the run's value range)
+        s.rte[r] = (lo < hi && j >= h0 && j != 0)
+                       ? (uint32_t)((lo - a0) << 16 | (hi - a0)) | ((rb < a0 || re > a0 + alen) ? 0x40000000u : 0u)
+                       : 0xffffffffu;
       }
     }
     __syncthreads();
@@ -990,24 +995,25 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ wcost) {
       }
       const uint32_t run = s.rte[lo];
       bool live = false;
-      uint32_t ps = 0, i = 0;
+      uint32_t ps = 0, i = 0, iend = 0;
       if (run != 0xffffffffu) {
-        if (pristine) {  // static {slot, row}: no dead / pos_of / erow gathers
+        if (pristine) {  // static {slot, row} and row end: no dead / pos_of / erow / row gathers
           const uint2 pv = a.pin_p[k];
           ps = pv.x, i = pv.y, live = true;
+          iend = a.pin_end[k];
         } else {
           const uint32_t id = a.pe[k];
           live = !y.dead[id];
-          if (live) ps = y.pos_of[id], i = y.erow[id];
+          if (live) {
+            ps = y.pos_of[id], i = y.erow[id];
+            iend = g.row_ptr[i] + g.deg[i];
+          }
         }
       }
       if (live) {
-        const uint32_t iend = g.row_ptr[i] + g.deg[i];
         uint32_t tlo = ps + 1, thi = iend;
-        const uint32_t tb = run >> 16, te = run & 0xffffu;
-        const uint32_t j = jf + lo;
-        const uint64_t rb = g.row_ptr[j];
-        if (rb < a0 || rb + g.deg[j] > a0 + alen) {  // partial run: clip the tail
+        const uint32_t tb = (run >> 16) & 0x3fffu, te = run & 0xffffu;
+        if (run & 0x40000000u) {  // partial run: clip the tail
           tlo = lb_global(col, tlo, thi, col[a0 + tb]);
           thi = lb_global(col, tlo, thi, col[a0 + te - 1] + 1);
         }
@@ -1096,7 +1102,7 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ wcost) {
       // (value, run) lookup of tail element c of pivot pp: the value may also
       // sit in other rows' runs
       auto probe = [&](uint32_t c, uint32_t slot, uint32_t run, uint32_t pp) {
-        const uint32_t tb = (run >> 16) & 0x7fffu, te = run & 0xffffu;
+        const uint32_t tb = (run >> 16) & 0x3fffu, te = run & 0xffffu;
         const uint32_t hh = a22_mix(c, te);
         const uint32_t fb = a22_fbit(hh);
         if (s.filt[fb >> 5] & (1u << (fb & 31))) {
@@ -2688,7 +2694,8 @@ __global__ void k_fill_all(const unsigned long long* __restrict__ keys, const ui
 __global__ void k_fill_in_all(const uint32_t* __restrict__ vkeys, const unsigned long long* __restrict__ vals,
                               uint64_t m, const unsigned long long* __restrict__ inoff,
                               const uint32_t* __restrict__ id_w, Sym y, uint32_t* __restrict__ pe,
-                              uint2* __restrict__ pin_p) {
+                              uint2* __restrict__ pin_p, uint32_t* __restrict__ pin_end,
+                              const uint32_t* __restrict__ row_ptr_w, const uint32_t* __restrict__ outdeg_w) {
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
     const uint32_t b = vkeys[i];
     const unsigned long long pv = vals[i];
@@ -2699,6 +2706,7 @@ __global__ void k_fill_in_all(const uint32_t* __restrict__ vkeys, const unsigned
     y.eid[dst] = id;
     pe[i] = id;
     pin_p[i] = make_uint2(slot, a);
+    pin_end[i] = row_ptr_w[a] + outdeg_w[a];
   }
 }
 
