@@ -1,0 +1,10 @@
+# final kernels: full suite (all reference digests), bench, ncu, launch list, sanitizers
+set -x
+mkdir -p gpurun_out
+timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/r02t_tests.log 2>&1
+python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r02t_smoke.log 2>&1
+timeout 1200 python bench.py > gpurun_out/r02t_bench.log 2>&1
+timeout 900 ncu --set full --import-source on --clock-control none -k regex:k_support_a22 -c 1 -o gpurun_out/r02t_a22_s24 python scripts/profile_run.py --scale 24 --k 3 --no-degree-bound > gpurun_out/r02t_ncu.log 2>&1
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/r02t_launch_s24.csv python scripts/profile_run.py --scale 24 --k 3 935 > gpurun_out/r02t_launch.log 2>&1
+rm -f gpurun_out/r02_san_summary.txt
+bash scripts/gpu_calls/r02_sanitize.sh
