@@ -561,7 +561,10 @@ __device__ __forceinline__ bool confirm(const Graph& g, SupportSmem& s, uint32_t
 //      red.add) and the pivot's count (smem); smem counts are flushed once.
 // Semantically each pivot slot gets exactly intersect_tails' matches
 // (support.cpp:64-91) plus the pivot add (support.cpp:122).
-__global__ void __launch_bounds__(kSupportThreads)
+#ifndef KTG_CHUNKED_MINB
+#define KTG_CHUNKED_MINB 1
+#endif
+__global__ void __launch_bounds__(kSupportThreads, KTG_CHUNKED_MINB)
 k_support_chunked(Graph g) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   SupportSmem& s = *reinterpret_cast<SupportSmem*>(smem_raw);
