@@ -562,7 +562,7 @@ __device__ __forceinline__ bool confirm(const Graph& g, SupportSmem& s, uint32_t
 // Semantically each pivot slot gets exactly intersect_tails' matches
 // (support.cpp:64-91) plus the pivot add (support.cpp:122).
 #ifndef KTG_CHUNKED_MINB
-#define KTG_CHUNKED_MINB 1
+#define KTG_CHUNKED_MINB 6  // 6 CTAs / SM at <= 40 registers: s24 pass 579 -> 379 ms (the 64-register build ran 4)
 #endif
 __global__ void __launch_bounds__(kSupportThreads, KTG_CHUNKED_MINB)
 k_support_chunked(Graph g) {
