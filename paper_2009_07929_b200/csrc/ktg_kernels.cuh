@@ -861,6 +861,9 @@ constexpr int kA22Batch = 256;
 #endif
 constexpr int kA22TableBits = 11;          // top hash bits when the table size is a power of two
 constexpr int kA22Strip = 256;             // flat tail elements a warp takes per grab
+#ifndef KTG_A22_STRIP_ADAPT
+#define KTG_A22_STRIP_ADAPT 1  // half strips when a batch has < 4 full strips per warp (balance at the barrier)
+#endif
 constexpr int kA22Table = KTG_A22_TABLE;     // slots (a power of two uses the top hash bits)
 constexpr int kA22Unroll = KTG_A22_UNROLL;     // tail elements per lane per step (loads in flight)
 constexpr int kA22FiltWords = 512;         // 16K filter bits for <= 512 entries (~3% false positives)
@@ -909,6 +912,33 @@ struct A22Smem {
   uint32_t next;
 };
 
+// Shared-memory accesses of the probe loop by 32-bit shared-window address
+// (base = the static A22Smem's cvta offset, a uniform constant). Through the
+// lambdas' generic references the compiler rebuilt the window base with an
+// S2R SR_CgaCtaId + LEA before every filter / table / counter access of the
+// probe path (20 S2R in the kernel, each a short-scoreboard round trip).
+#ifndef KTG_A22_ASMSMEM
+#define KTG_A22_ASMSMEM 1
+#endif
+// The static A22Smem is the kernel's only shared variable: it starts right
+// after the 1 KB the hardware reserves, and a launch without clusters has CTA
+// id 0 in its cluster, so its shared-window address is this constant (the
+// kernel traps if not). A literal keeps the compiler from rebuilding it.
+constexpr uint32_t kA22SmemBase = 0x400;
+__device__ __forceinline__ uint32_t lds_u32(uint32_t a) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ uint2 lds_v2(uint32_t a) {
+  uint2 v;
+  asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void reds_inc(uint32_t a) {
+  asm volatile("red.shared.add.u32 [%0], 1;" ::"r"(a) : "memory");
+}
+
 // One multiplicative hash of (value, run end): the table slot takes its top
 // kA22TableBits bits, the filter bit a fold of the rest.
 __device__ __forceinline__ uint32_t a22_mix(uint32_t v, uint32_t te) {
@@ -937,6 +967,9 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ wcost) {
   // static (not dynamic) shared memory: constant-offset LDS addressing
   __shared__ __align__(16) A22Smem s;
   const uint32_t tid = threadIdx.x;
+#if KTG_A22_ASMSMEM
+  if (tid == 0 && (uint32_t)__cvta_generic_to_shared(&s) != kA22SmemBase) __trap();
+#endif
   const int lane = tid & 31, wid = tid >> 5;
   constexpr int NW = kSupportThreads / 32;
   constexpr int EPT = kChunk / kSupportThreads;
@@ -1088,10 +1121,12 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ wcost) {
     uint32_t tri_task = 0;
     for (;;) {
       uint32_t base = 0;
-      if (lane == 0) base = atomicAdd(&s.next, (uint32_t)kA22Strip);
+      // (short batches: half strips, so the 8 warps reach the barrier together)
+      const uint32_t strip = (KTG_A22_STRIP_ADAPT && W < 4u * NW * kA22Strip) ? kA22Strip / 2 : kA22Strip;
+      if (lane == 0) base = atomicAdd(&s.next, strip);
       base = __shfl_sync(0xffffffffu, base, 0);
       if (base >= W) break;
-      const uint32_t lim = min(base + (uint32_t)kA22Strip, W);
+      const uint32_t lim = min(base + strip, W);
       // pivot holding base: p = #{q in [1, kA22Batch) : pref[q] <= base}
       // (pref ascends), two ballots over groups of 8 instead of a search
       static_assert(kA22Batch == 256, "two-level ballot assumes 32 groups of 8");
@@ -1102,6 +1137,47 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ wcost) {
         p = 8 * g + c2;
       }
       uint32_t pe_ = s.pref[p + 1], pb = s.pref[p], plo = s.plo[p], prun = s.prun[p];
+#if KTG_A22_ASMSMEM
+      constexpr uint32_t sb = kA22SmemBase;  // checked against &s at kernel entry
+      constexpr uint32_t oF = offsetof(A22Smem, filt), oT = offsetof(A22Smem, tab), oA = offsetof(A22Smem, cntA),
+                         oP = offsetof(A22Smem, cntP), oR = offsetof(A22Smem, pref), oL = offsetof(A22Smem, plo),
+                         oU = offsetof(A22Smem, prun);
+      auto probe = [&](uint32_t c, uint32_t slot, uint32_t run, uint32_t pp) {
+        const uint32_t tb = (run >> 16) & 0x3fffu, te = run & 0xffffu;
+        const uint32_t hh = a22_mix(c, te);
+        const uint32_t fb = a22_fbit(hh);
+        if (lds_u32(sb + oF + ((fb >> 5) << 2)) & (1u << (fb & 31))) {
+          uint32_t x = kChunk;
+          for (uint32_t h = a22_slot(hh);; h = a22_next(h)) {
+            const uint2 e = lds_v2(sb + oT + (h << 3));
+            if (e.x == 0) break;
+            if (e.x == c && e.y - tb < te - tb) {
+              x = e.y;
+              break;
+            }
+          }
+          if (x < (uint32_t)kChunk) {
+            reds_inc(sb + oA + (x << 2));
+            if (!KTG_A22_LIGHT || !(run >> 31)) {
+              atomicAdd(&S[slot], 1u);
+              reds_inc(sb + oP + (pp << 2));
+            }
+            ++tri_task;
+          }
+        }
+      };
+      auto advance = [&](uint32_t f) {
+        if (f >= pe_) {
+          do {
+            ++p;
+            pe_ = lds_u32(sb + oR + ((p + 1) << 2));
+          } while (pe_ <= f);
+          pb = lds_u32(sb + oR + (p << 2));
+          plo = lds_u32(sb + oL + (p << 2));
+          prun = lds_u32(sb + oU + (p << 2));
+        }
+      };
+#else
       // (value, run) lookup of tail element c of pivot pp: the value may also
       // sit in other rows' runs
       auto probe = [&](uint32_t c, uint32_t slot, uint32_t run, uint32_t pp) {
@@ -1139,6 +1215,7 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ wcost) {
           prun = s.prun[p];
         }
       };
+#endif
       // kA22Unroll elements per lane per step, every load issued before any probe
       for (uint32_t f = base + lane; f < lim; f += 32 * kA22Unroll) {
         uint32_t sl[kA22Unroll], ru[kA22Unroll], pv[kA22Unroll], cv[kA22Unroll];

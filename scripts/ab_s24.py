@@ -9,16 +9,17 @@ import paper_2009_07929_b200 as kt
 
 ap = argparse.ArgumentParser()
 ap.add_argument("--scale", type=int, default=24)
+ap.add_argument("--graph", default="rmat", choices=["rmat", "er"])
 ap.add_argument("--cache", default="/tmp/ktg_s24.ztcsr")
 ap.add_argument("--ks", default="3,935")
 ap.add_argument("--tag", default=os.environ.get("KTG_LIB_DIR", "lib"))
 ap.add_argument("--recompute", action="store_true", help="KTG_FLAG_RECOMPUTE engines (k_support_chunked)")
 a = ap.parse_args()
 if not os.path.exists(a.cache):
-    g = kt.rmat(a.scale)
+    g = kt.rmat(a.scale) if a.graph == "rmat" else kt.erdos_renyi(a.scale, 16 << a.scale)
     kt.graph.write_csr_cache(g, a.cache)
 g = kt.graph.read_csr_cache(a.cache)
-out = {"tag": a.tag}
+out = {"tag": a.tag, "graph": f"{a.graph}{a.scale}"}
 e = kt.Engine(g, kt.TrussOptions(recompute=True) if a.recompute else kt.TrussOptions(no_degree_bound=True),
               time_support=True)
 best = 1e9
