@@ -500,6 +500,23 @@ ktg_status prepare_layout(ktg_engine* e, Layout& L, bool keep_pristine, const ui
   return KTG_OK;
 }
 
+// KTG_LOAD_TIMING=1: per-phase wall times of the host-buffer path on stderr
+// (debug; synchronises the stream at every mark, so never on in a benchmark).
+struct PhaseTimer {
+  cudaStream_t s;
+  bool on;
+  double last = 0;
+  explicit PhaseTimer(cudaStream_t st) : s(st), on(getenv("KTG_LOAD_TIMING") != nullptr) {}
+  void operator()(const char* what) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    const double now =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
+    if (last != 0) fprintf(stderr, "ktg: %-28s %8.3f ms\n", what, now - last);
+    last = now;
+  }
+};
+
 ktg_status sym_alloc(ktg_engine* e, uint64_t m);
 
 // Degree-ordered working layout from the caller layout's current state; with
@@ -533,6 +550,8 @@ ktg_status build_working(ktg_engine* e, bool with_sym) {
   KTG_CUDA(cudaMemsetAsync(e->din.p, 0, nb * 4, s));
   KTG_CUDA(cudaMemsetAsync(e->cntw.p, 0, nb * 4, s));
   KTG_CUDA(cudaMemsetAsync(e->symdeg_w.p, 0, nb * 4, s));
+  PhaseTimer mk(s);
+  mk("bw start");
   k_work_din<<<e->prune_grid, kPruneThreads, 0, s>>>(g, e->din.p);
   k_rank_keys<<<4 * e->num_sms, 256, 0, s>>>(C.deg.p, e->din.p, n, e->keys.p);
   KTG_CUDA(cudaGetLastError());
@@ -562,6 +581,7 @@ ktg_status build_working(ktg_engine* e, bool with_sym) {
   KTG_CUDA(cub::DeviceRadixSort::SortKeys(e->cub_tmp.p, tmp, e->keys.p, e->keys_sorted.p, (int)n, 0,
                                           32 + deg_bits, s));
   k_rank_assign<<<4 * e->num_sms, 256, 0, s>>>(e->keys_sorted.p, n, e->rank.p, e->symdeg_w.p);
+  mk("bw: degrees + rank sort");
   // edge keys in caller row order, then sort by (a, b)
   tmp = e->cub_tmp.cap;
   KTG_CUDA(cub::DeviceScan::ExclusiveSum(e->cub_tmp.p, tmp, C.deg.p, e->offs.p, (int)nb, s));
@@ -574,9 +594,11 @@ ktg_status build_working(ktg_engine* e, bool with_sym) {
   k_edge_keys<<<e->prune_grid, kPruneThreads, 0, s>>>(g, e->rank.p, e->offs.p, B, e->keys.p, e->vals.p,
                                                       with_sym ? e->erow.p : nullptr);
   KTG_CUDA(cudaGetLastError());
+  mk("bw: edge keys");
   tmp = e->cub_tmp.cap;
   KTG_CUDA(cub::DeviceRadixSort::SortPairs(e->cub_tmp.p, tmp, e->keys.p, e->keys_sorted.p, e->vals.p,
                                            e->vals_sorted.p, (int64_t)m, 0, 2 * B, s));
+  mk("bw: (a, b) sort");
   k_run_counts<<<(n + 255) / 256, 256, 0, s>>>(e->keys_sorted.p, m, n, B, e->cntw.p);
   // working row_ptr = exclusive scan of (out-degree + sentinel)
   k_row_sizes<<<4 * e->num_sms, 256, 0, s>>>(e->cntw.p, n, e->sizes.p);
@@ -584,6 +606,7 @@ ktg_status build_working(ktg_engine* e, bool with_sym) {
   KTG_CUDA(cub::DeviceScan::ExclusiveSum(e->cub_tmp.p, tmp, e->sizes.p, W.row_ptr.p, (int)nb, s));
   KTG_CUDA(cudaMemsetAsync(W.col.p, 0, W.slots * 4, s));
   KTG_CUDA(cudaMemsetAsync(W.id.p, 0, W.slots * 4, s));  // sentinel slots carry id 0 (initcheck-clean copies)
+  mk("bw: row sizes + scan");
   if (!with_sym) {
     k_fill_working<<<8 * e->num_sms, 256, 0, s>>>(e->keys_sorted.p, e->vals_sorted.p, m, B, W.col.p, W.id.p);
     KTG_CUDA(cudaGetLastError());
@@ -601,15 +624,20 @@ ktg_status build_working(ktg_engine* e, bool with_sym) {
                                             W.id.p, e->din.p, e->symdeg_w.p, y, e->vals.p, e->keys.p,
                                             e->d_workL);
   KTG_CUDA(cudaGetLastError());
+  mk("bw: fill rows + sym");
   tmp = e->cub_tmp.cap;
   KTG_CUDA(cub::DeviceRadixSort::SortPairs(e->cub_tmp.p, tmp, e->vals.p, e->vals_sorted.p, e->keys.p,
                                            e->keys_sorted.p, (int64_t)m, 0, (int)B, s));
+  mk("bw: in-list sort");
   k_fill_in_all<<<8 * e->num_sms, 256, 0, s>>>(e->vals_sorted.p, e->keys_sorted.p, m, sz + 3 * nb, W.id.p, y,
                                                e->a22_pe.p, e->a22_pin.p, e->a22_pin_end.p, W.row_ptr.p,
                                                e->cntw.p);
   KTG_CUDA(cudaGetLastError());
   KTG_CUDA(cudaMemcpyAsync(e->sym_deg.p, e->symdeg_w.p, nb * 4, cudaMemcpyDeviceToDevice, s));
-  return prepare_layout(e, W, true, e->cntw.p, m);
+  mk("bw: in-list fill");
+  const ktg_status pst = prepare_layout(e, W, true, e->cntw.p, m);
+  mk("bw: prepare working layout");
+  return pst;
 }
 
 // Static structures of the A22-staged support pass (after build_sym): the
@@ -754,22 +782,6 @@ ktg_status build_sym(ktg_engine* e) {
   return build_a22(e);
 }
 
-// KTG_LOAD_TIMING=1: per-phase wall times of the host-buffer path on stderr
-// (debug; synchronises the stream at every mark, so never on in a benchmark).
-struct PhaseTimer {
-  cudaStream_t s;
-  bool on;
-  double last = 0;
-  explicit PhaseTimer(cudaStream_t st) : s(st), on(getenv("KTG_LOAD_TIMING") != nullptr) {}
-  void operator()(const char* what) {
-    if (!on) return;
-    cudaStreamSynchronize(s);
-    const double now =
-        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch()).count();
-    if (last != 0) fprintf(stderr, "ktg: %-28s %8.3f ms\n", what, now - last);
-    last = now;
-  }
-};
 
 // Uploads (host or device source) into the caller layout; builds the working
 // layout unless the label order is requested. Buffers are reused when the

@@ -953,6 +953,29 @@ __device__ __forceinline__ uint32_t a22_next(uint32_t h) {
   return h + 1 == (uint32_t)kA22Table ? 0u : h + 1;
 }
 __device__ __forceinline__ uint32_t a22_fbit(uint32_t h) { return (h ^ (h >> 15)) & (kA22FiltWords * 32 - 1); }
+// KTG_A22_HASH2: the same (value, run end) key hashed with one IMAD per tail
+// element. The run word's contribution rk = run * kA22RunMul keeps only the
+// run end te (bits 0-15: kA22RunMul is a multiple of 2^16, so the tb / flag
+// bits vanish) and is formed once per pivot in the advance; h = c * kA22Mul +
+// rk. Filter word = top 9 bits, bit 31 - (h & 31) (the funnel shift's own wrap); the
+// positive path re-reads the pivot's run word for tb / te / the light flag.
+// (The old mix: 4 instructions for the key, 6 for the filter bit.)
+#ifndef KTG_A22_HASH2
+#define KTG_A22_HASH2 1
+#endif
+#ifndef KTG_A22_FAST
+#define KTG_A22_FAST KTG_A22_HASH2  // warp-uniform fast path for windows inside one pivot's tail
+#endif
+#if KTG_A22_FAST && !KTG_A22_HASH2
+#error "KTG_A22_FAST needs KTG_A22_HASH2"
+#endif
+#if KTG_A22_HASH2 && !KTG_A22_ASMSMEM
+#error "KTG_A22_HASH2 is implemented on the KTG_A22_ASMSMEM probe path"
+#endif
+constexpr uint32_t kA22Mul = 2654435761u;
+constexpr uint32_t kA22RunMul = ((0x85EBCA6Bu * 2654435761u) & 0xffffu) << 16;  // odd << 16: te -> bijective offset
+static_assert(kA22FiltWords == 512, "HASH2 takes the filter word from the top 9 hash bits");
+__device__ __forceinline__ uint32_t a22_h2(uint32_t v, uint32_t rk) { return v * kA22Mul + rk; }
 
 // COST = true (multi-rank runs, before every full pass): steps 1-2 only, over
 // all tasks; wcost[t] = the task's flattened tail work W, the weights of the
@@ -1106,9 +1129,14 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ wcost) {
         const uint32_t v = s.A[x];
         if (x < alen && v == 0) cur = x;
         if (v != 0) {  // claim the first free slot from home (values are >= 1)
+#if KTG_A22_HASH2
+          const uint32_t hh = a22_h2(v, cur * kA22RunMul);
+          atomicOr(&s.filt[hh >> 23], 0x80000000u >> (hh & 31));
+#else
           const uint32_t hh = a22_mix(v, cur);
           const uint32_t fb = a22_fbit(hh);
           atomicOr(&s.filt[fb >> 5], 1u << (fb & 31));
+#endif
           uint32_t h = a22_slot(hh);
           while (atomicCAS(&s.tab[h].x, 0u, v) != 0u) h = a22_next(h);
           s.tab[h].y = x;
@@ -1142,11 +1170,20 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ wcost) {
       constexpr uint32_t oF = offsetof(A22Smem, filt), oT = offsetof(A22Smem, tab), oA = offsetof(A22Smem, cntA),
                          oP = offsetof(A22Smem, cntP), oR = offsetof(A22Smem, pref), oL = offsetof(A22Smem, plo),
                          oU = offsetof(A22Smem, prun);
+#if KTG_A22_HASH2
+      // table probe of a filter hit: tail element c (hash hh) of pivot pp,
+      // whose run word is re-read here (the step loop carries only rk)
+      auto probe = [&](uint32_t c, uint32_t slot, uint32_t hh, uint32_t pp) {
+        {
+          const uint32_t run = lds_u32(sb + oU + (pp << 2));
+          const uint32_t tb = (run >> 16) & 0x3fffu, te = run & 0xffffu;
+#else
       auto probe = [&](uint32_t c, uint32_t slot, uint32_t run, uint32_t pp) {
         const uint32_t tb = (run >> 16) & 0x3fffu, te = run & 0xffffu;
         const uint32_t hh = a22_mix(c, te);
         const uint32_t fb = a22_fbit(hh);
         if (lds_u32(sb + oF + ((fb >> 5) << 2)) & (1u << (fb & 31))) {
+#endif
           uint32_t x = kChunk;
           for (uint32_t h = a22_slot(hh);; h = a22_next(h)) {
             const uint2 e = lds_v2(sb + oT + (h << 3));
@@ -1175,8 +1212,14 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ wcost) {
           pb = lds_u32(sb + oR + (p << 2));
           plo = lds_u32(sb + oL + (p << 2));
           prun = lds_u32(sb + oU + (p << 2));
+#if KTG_A22_HASH2
+          prun *= kA22RunMul;
+#endif
         }
       };
+#if KTG_A22_HASH2
+      prun *= kA22RunMul;  // from here on prun holds the pivot's rk
+#endif
 #else
       // (value, run) lookup of tail element c of pivot pp: the value may also
       // sit in other rows' runs
@@ -1216,8 +1259,31 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ wcost) {
         }
       };
 #endif
-      // kA22Unroll elements per lane per step, every load issued before any probe
-      for (uint32_t f = base + lane; f < lim; f += 32 * kA22Unroll) {
+      // kA22Unroll elements per lane per step, every load issued before any
+      // probe (warp-uniform loop: lanes past lim carry out-of-range elements)
+      for (uint32_t f0 = base; f0 < lim; f0 += 32 * kA22Unroll) {
+        const uint32_t f = f0 + lane;
+#if KTG_A22_FAST
+        // every lane's window of kA22Unroll elements inside its current
+        // pivot's tail (long tails, most of the elements): no per-element
+        // pivot advance, range checks or per-element pivot state
+        if (__all_sync(0xffffffffu, f + 32 * (kA22Unroll - 1) < min(pe_, lim))) {
+          const uint32_t s0 = plo + (f - pb);
+          uint32_t cv[kA22Unroll], hv[kA22Unroll];
+#pragma unroll
+          for (int u = 0; u < kA22Unroll; ++u) cv[u] = col[s0 + 32 * u];
+#pragma unroll
+          for (int u = 0; u < kA22Unroll; ++u) hv[u] = a22_h2(cv[u], prun);
+          bool hit[kA22Unroll];
+#pragma unroll
+          for (int u = 0; u < kA22Unroll; ++u)
+            hit[u] = (int32_t)__funnelshift_l(0u, lds_u32(sb + oF + ((hv[u] >> 23) << 2)), hv[u]) < 0;
+#pragma unroll
+          for (int u = 0; u < kA22Unroll; ++u)
+            if (hit[u]) probe(cv[u], s0 + 32 * u, hv[u], p);
+          continue;
+        }
+#endif
         uint32_t sl[kA22Unroll], ru[kA22Unroll], pv[kA22Unroll], cv[kA22Unroll];
 #pragma unroll
         for (int u = 0; u < kA22Unroll; ++u) {
@@ -1227,9 +1293,26 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ wcost) {
         }
 #pragma unroll
         for (int u = 0; u < kA22Unroll; ++u) cv[u] = (f + 32 * u < lim) ? col[sl[u]] : 0u;
+#if KTG_A22_HASH2
+        // the kA22Unroll hashes and filter reads as independent chains (the
+        // filter bit 31 - (h & 31) lands in the sign: one funnel shift and a
+        // sign test); only the hits branch into the table probe
+#pragma unroll
+        for (int u = 0; u < kA22Unroll; ++u) ru[u] = a22_h2(cv[u], ru[u]);
+        bool hit[kA22Unroll];
+#pragma unroll
+        for (int u = 0; u < kA22Unroll; ++u) {
+          const uint32_t w = lds_u32(sb + oF + ((ru[u] >> 23) << 2));
+          hit[u] = f + 32 * u < lim && (int32_t)__funnelshift_l(0u, w, ru[u]) < 0;
+        }
+#pragma unroll
+        for (int u = 0; u < kA22Unroll; ++u)
+          if (hit[u]) probe(cv[u], sl[u], ru[u], pv[u]);
+#else
 #pragma unroll
         for (int u = 0; u < kA22Unroll; ++u)
           if (f + 32 * u < lim) probe(cv[u], sl[u], ru[u], pv[u]);
+#endif
       }
     }
     tri_local += tri_task;
@@ -2720,6 +2803,11 @@ __global__ void k_fill_working(const unsigned long long* __restrict__ keys, cons
   }
 }
 
+#ifndef KTG_FILL_UNROLL
+#define KTG_FILL_UNROLL 4
+#endif
+constexpr int kFillUnroll = KTG_FILL_UNROLL;  // load-time fill passes: entries per thread per step
+
 // Working layout + symmetric rows in one pass (carried-support runs): per
 // rank r, din_w = undirected degree - out-degree; the u64 sizes for the
 // symmetric-row offsets (tot | din) scans.
@@ -2748,20 +2836,48 @@ __global__ void k_fill_all(const unsigned long long* __restrict__ keys, const ui
                            unsigned long long* __restrict__ ivals, unsigned long long* __restrict__ cap) {
   const unsigned long long mask = (1ull << B) - 1;
   unsigned long long c = 0;
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
-    const unsigned long long k = keys[i];
-    const uint32_t a = (uint32_t)(k >> B), b = (uint32_t)(k & mask);
-    const uint32_t id = vals[i];
-    const uint32_t slot = (uint32_t)(i + a - 1);
-    col_w[slot] = b;
-    id_w[slot] = id;
-    y.pos_of[id] = slot;  // erow[id] = a was written by k_edge_keys
-    const unsigned long long dst = y.ptr[a] + din_w[a] + (slot - row_ptr_w[a]);
-    y.nbr[dst] = b;
-    y.eid[dst] = id;
-    ikeys[i] = b;
-    ivals[i] = ((unsigned long long)a << 32) | slot;
-    c += (min(symdeg_w[a], symdeg_w[b]) + kDeltaPiece - 1) / kDeltaPiece;
+  // kFillUnroll entries per thread per step, each phase's loads issued for
+  // all of them before any use (the pass is latency-bound on the per-row
+  // gathers and the scattered pos_of store, not on its streaming bytes)
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i0 < m; i0 += kFillUnroll * stride) {
+    unsigned long long k[kFillUnroll];
+    uint32_t id[kFillUnroll], a[kFillUnroll], b[kFillUnroll];
+#pragma unroll
+    for (int u = 0; u < kFillUnroll; ++u) {
+      const uint64_t i = i0 + u * stride;
+      k[u] = i < m ? keys[i] : 0ull;
+      id[u] = i < m ? vals[i] : 0u;
+    }
+#pragma unroll
+    for (int u = 0; u < kFillUnroll; ++u) a[u] = (uint32_t)(k[u] >> B), b[u] = (uint32_t)(k[u] & mask);
+    unsigned long long base[kFillUnroll];
+    uint32_t rw[kFillUnroll], da[kFillUnroll], db[kFillUnroll];
+#pragma unroll
+    for (int u = 0; u < kFillUnroll; ++u) {
+      if (i0 + u * stride < m) {
+        base[u] = y.ptr[a[u]] + din_w[a[u]];
+        rw[u] = row_ptr_w[a[u]];
+        da[u] = symdeg_w[a[u]];
+        db[u] = symdeg_w[b[u]];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kFillUnroll; ++u) {
+      const uint64_t i = i0 + u * stride;
+      if (i < m) {
+        const uint32_t slot = (uint32_t)(i + a[u] - 1);
+        col_w[slot] = b[u];
+        id_w[slot] = id[u];
+        y.pos_of[id[u]] = slot;  // erow[id] = a was written by k_edge_keys
+        const unsigned long long dst = base[u] + (slot - rw[u]);
+        y.nbr[dst] = b[u];
+        y.eid[dst] = id[u];
+        ikeys[i] = b[u];
+        ivals[i] = ((unsigned long long)a[u] << 32) | slot;
+        c += (min(da[u], db[u]) + kDeltaPiece - 1) / kDeltaPiece;
+      }
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
@@ -2776,17 +2892,39 @@ __global__ void k_fill_in_all(const uint32_t* __restrict__ vkeys, const unsigned
                               const uint32_t* __restrict__ id_w, Sym y, uint32_t* __restrict__ pe,
                               uint2* __restrict__ pin_p, uint32_t* __restrict__ pin_end,
                               const uint32_t* __restrict__ row_ptr_w, const uint32_t* __restrict__ outdeg_w) {
-  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < m; i += (uint64_t)gridDim.x * blockDim.x) {
-    const uint32_t b = vkeys[i];
-    const unsigned long long pv = vals[i];
-    const uint32_t a = (uint32_t)(pv >> 32), slot = (uint32_t)pv;
-    const uint32_t id = id_w[slot];
-    const unsigned long long dst = y.ptr[b] + (i - inoff[b]);
-    y.nbr[dst] = a;
-    y.eid[dst] = id;
-    pe[i] = id;
-    pin_p[i] = make_uint2(slot, a);
-    pin_end[i] = row_ptr_w[a] + outdeg_w[a];
+  const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
+  for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i0 < m; i0 += kFillUnroll * stride) {
+    uint32_t b[kFillUnroll], a[kFillUnroll], slot[kFillUnroll];
+#pragma unroll
+    for (int u = 0; u < kFillUnroll; ++u) {
+      const uint64_t i = i0 + u * stride;
+      unsigned long long pv = 0;
+      b[u] = 0;
+      if (i < m) b[u] = vkeys[i], pv = vals[i];
+      a[u] = (uint32_t)(pv >> 32), slot[u] = (uint32_t)pv;
+    }
+    uint32_t id[kFillUnroll], end[kFillUnroll];
+    unsigned long long dst[kFillUnroll];
+#pragma unroll
+    for (int u = 0; u < kFillUnroll; ++u) {
+      const uint64_t i = i0 + u * stride;
+      if (i < m) {
+        id[u] = id_w[slot[u]];
+        dst[u] = y.ptr[b[u]] + (i - inoff[b[u]]);
+        end[u] = row_ptr_w[a[u]] + outdeg_w[a[u]];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < kFillUnroll; ++u) {
+      const uint64_t i = i0 + u * stride;
+      if (i < m) {
+        y.nbr[dst[u]] = a[u];
+        y.eid[dst[u]] = id[u];
+        pe[i] = id[u];
+        pin_p[i] = make_uint2(slot[u], a[u]);
+        pin_end[i] = end[u];
+      }
+    }
   }
 }
 
