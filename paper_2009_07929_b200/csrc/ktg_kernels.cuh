@@ -963,12 +963,10 @@ __device__ __forceinline__ uint32_t a22_fbit(uint32_t h) { return (h ^ (h >> 15)
 #ifndef KTG_A22_HASH2
 #define KTG_A22_HASH2 1
 #endif
-#ifndef KTG_A22_FAST
-#define KTG_A22_FAST KTG_A22_HASH2  // warp-uniform fast path for windows inside one pivot's tail
+#ifndef KTG_A22_FULLSTRIP
+#define KTG_A22_FULLSTRIP 1  // whole strips step without per-element range checks
 #endif
-#if KTG_A22_FAST && !KTG_A22_HASH2
-#error "KTG_A22_FAST needs KTG_A22_HASH2"
-#endif
+static_assert(kA22Strip % (2 * 32 * kA22Unroll) == 0, "full and half strips are whole steps");
 #if KTG_A22_HASH2 && !KTG_A22_ASMSMEM
 #error "KTG_A22_HASH2 is implemented on the KTG_A22_ASMSMEM probe path"
 #endif
@@ -1139,7 +1137,13 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ wcost) {
 #endif
           uint32_t h = a22_slot(hh);
           while (atomicCAS(&s.tab[h].x, 0u, v) != 0u) h = a22_next(h);
+#if KTG_A22_HASH2
+          // payload: x's byte offset in cntA | its run's rk (te * kA22RunMul,
+          // bits 16-31) -- a probe matches on (value, rk) without the run bounds
+          s.tab[h].y = (x << 2) | (cur * kA22RunMul);
+#else
           s.tab[h].y = x;
+#endif
         }
       }
     }
@@ -1171,19 +1175,32 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ wcost) {
                          oP = offsetof(A22Smem, cntP), oR = offsetof(A22Smem, pref), oL = offsetof(A22Smem, plo),
                          oU = offsetof(A22Smem, prun);
 #if KTG_A22_HASH2
-      // table probe of a filter hit: tail element c (hash hh) of pivot pp,
-      // whose run word is re-read here (the step loop carries only rk)
-      auto probe = [&](uint32_t c, uint32_t slot, uint32_t hh, uint32_t pp) {
-        {
-          const uint32_t run = lds_u32(sb + oU + (pp << 2));
-          const uint32_t tb = (run >> 16) & 0x3fffu, te = run & 0xffffu;
+      // table probe of a filter hit: tail element c (hash hh) of the pivot
+      // pl (index | light flag << 31). The entry matches on its value and its
+      // run's rk = hh - c * kA22Mul: inside one chunk a value's run end
+      // identifies its row (runs are the maximal nonzero stretches). The
+      // triangle count comes from the cntA flush.
+      auto probe = [&](uint32_t c, uint32_t slot, uint32_t hh, uint32_t pl) {
+        const uint32_t rk = hh - c * kA22Mul;
+        for (uint32_t h = a22_slot(hh);; h = a22_next(h)) {
+          const uint2 e = lds_v2(sb + oT + (h << 3));
+          if (e.x == 0) break;
+          if (e.x == c && (e.y ^ rk) < 0x10000u) {
+            reds_inc(sb + oA + (e.y & 0xffffu));
+            if (!KTG_A22_LIGHT || (int32_t)pl >= 0) {
+              atomicAdd(&S[slot], 1u);
+              reds_inc(sb + oP + (pl << 2));  // (the flag shifts out)
+            }
+            break;
+          }
+        }
+      };
 #else
       auto probe = [&](uint32_t c, uint32_t slot, uint32_t run, uint32_t pp) {
         const uint32_t tb = (run >> 16) & 0x3fffu, te = run & 0xffffu;
         const uint32_t hh = a22_mix(c, te);
         const uint32_t fb = a22_fbit(hh);
         if (lds_u32(sb + oF + ((fb >> 5) << 2)) & (1u << (fb & 31))) {
-#endif
           uint32_t x = kChunk;
           for (uint32_t h = a22_slot(hh);; h = a22_next(h)) {
             const uint2 e = lds_v2(sb + oT + (h << 3));
@@ -1203,6 +1220,27 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ wcost) {
           }
         }
       };
+#endif
+#if KTG_A22_HASH2
+      // p carries the pivot's light flag in bit 31 (its run word's bit 31:
+      // round-0 rows below h0) and prun the pivot's rk from here on
+      p |= prun & 0x80000000u;
+      prun *= kA22RunMul;
+      auto advance = [&](uint32_t f) {
+        if (f >= pe_) {
+          p &= 0x7fffffffu;
+          do {
+            ++p;
+            pe_ = lds_u32(sb + oR + ((p + 1) << 2));
+          } while (pe_ <= f);
+          pb = lds_u32(sb + oR + (p << 2));
+          plo = lds_u32(sb + oL + (p << 2));
+          prun = lds_u32(sb + oU + (p << 2));
+          p |= prun & 0x80000000u;
+          prun *= kA22RunMul;
+        }
+      };
+#else
       auto advance = [&](uint32_t f) {
         if (f >= pe_) {
           do {
@@ -1212,13 +1250,8 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ wcost) {
           pb = lds_u32(sb + oR + (p << 2));
           plo = lds_u32(sb + oL + (p << 2));
           prun = lds_u32(sb + oU + (p << 2));
-#if KTG_A22_HASH2
-          prun *= kA22RunMul;
-#endif
         }
       };
-#if KTG_A22_HASH2
-      prun *= kA22RunMul;  // from here on prun holds the pivot's rk
 #endif
 #else
       // (value, run) lookup of tail element c of pivot pp: the value may also
@@ -1259,41 +1292,19 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ wcost) {
         }
       };
 #endif
-      // kA22Unroll elements per lane per step, every load issued before any
-      // probe (warp-uniform loop: lanes past lim carry out-of-range elements)
-      for (uint32_t f0 = base; f0 < lim; f0 += 32 * kA22Unroll) {
-        const uint32_t f = f0 + lane;
-#if KTG_A22_FAST
-        // every lane's window of kA22Unroll elements inside its current
-        // pivot's tail (long tails, most of the elements): no per-element
-        // pivot advance, range checks or per-element pivot state
-        if (__all_sync(0xffffffffu, f + 32 * (kA22Unroll - 1) < min(pe_, lim))) {
-          const uint32_t s0 = plo + (f - pb);
-          uint32_t cv[kA22Unroll], hv[kA22Unroll];
-#pragma unroll
-          for (int u = 0; u < kA22Unroll; ++u) cv[u] = col[s0 + 32 * u];
-#pragma unroll
-          for (int u = 0; u < kA22Unroll; ++u) hv[u] = a22_h2(cv[u], prun);
-          bool hit[kA22Unroll];
-#pragma unroll
-          for (int u = 0; u < kA22Unroll; ++u)
-            hit[u] = (int32_t)__funnelshift_l(0u, lds_u32(sb + oF + ((hv[u] >> 23) << 2)), hv[u]) < 0;
-#pragma unroll
-          for (int u = 0; u < kA22Unroll; ++u)
-            if (hit[u]) probe(cv[u], s0 + 32 * u, hv[u], p);
-          continue;
-        }
-#endif
+      // kA22Unroll elements per lane per step, every load issued before any probe
+#if KTG_A22_HASH2
+      // full: every element of the step is inside the strip (no range checks)
+      auto step = [&](const uint32_t f, const bool full) {
         uint32_t sl[kA22Unroll], ru[kA22Unroll], pv[kA22Unroll], cv[kA22Unroll];
 #pragma unroll
         for (int u = 0; u < kA22Unroll; ++u) {
           const uint32_t fu = f + 32 * u;
-          if (fu < lim) advance(fu);
+          if (full || fu < lim) advance(fu);
           sl[u] = plo + (fu - pb), ru[u] = prun, pv[u] = p;
         }
 #pragma unroll
-        for (int u = 0; u < kA22Unroll; ++u) cv[u] = (f + 32 * u < lim) ? col[sl[u]] : 0u;
-#if KTG_A22_HASH2
+        for (int u = 0; u < kA22Unroll; ++u) cv[u] = (full || f + 32 * u < lim) ? col[sl[u]] : 0u;
         // the kA22Unroll hashes and filter reads as independent chains (the
         // filter bit 31 - (h & 31) lands in the sign: one funnel shift and a
         // sign test); only the hits branch into the table probe
@@ -1303,27 +1314,46 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ wcost) {
 #pragma unroll
         for (int u = 0; u < kA22Unroll; ++u) {
           const uint32_t w = lds_u32(sb + oF + ((ru[u] >> 23) << 2));
-          hit[u] = f + 32 * u < lim && (int32_t)__funnelshift_l(0u, w, ru[u]) < 0;
+          hit[u] = (full || f + 32 * u < lim) && (int32_t)__funnelshift_l(0u, w, ru[u]) < 0;
         }
 #pragma unroll
         for (int u = 0; u < kA22Unroll; ++u)
           if (hit[u]) probe(cv[u], sl[u], ru[u], pv[u]);
+      };
+#if KTG_A22_FULLSTRIP
+      if (lim - base == strip) {  // a whole strip (strip is a multiple of 32 * kA22Unroll)
+        for (uint32_t f = base + lane; f < lim; f += 32 * kA22Unroll) step(f, true);
+      } else
+#endif
+        for (uint32_t f = base + lane; f < lim; f += 32 * kA22Unroll) step(f, false);
 #else
+      for (uint32_t f = base + lane; f < lim; f += 32 * kA22Unroll) {
+        uint32_t sl[kA22Unroll], ru[kA22Unroll], pv[kA22Unroll], cv[kA22Unroll];
+#pragma unroll
+        for (int u = 0; u < kA22Unroll; ++u) {
+          const uint32_t fu = f + 32 * u;
+          if (fu < lim) advance(fu);
+          sl[u] = plo + (fu - pb), ru[u] = prun, pv[u] = p;
+        }
+#pragma unroll
+        for (int u = 0; u < kA22Unroll; ++u) cv[u] = (f + 32 * u < lim) ? col[sl[u]] : 0u;
 #pragma unroll
         for (int u = 0; u < kA22Unroll; ++u)
           if (f + 32 * u < lim) probe(cv[u], sl[u], ru[u], pv[u]);
-#endif
       }
+#endif
     }
     tri_local += tri_task;
     __syncthreads();
 
-    // 5. flush shared counts (A22 slots, pivots)
+    // 5. flush shared counts (A22 slots, pivots); every triangle found bumped
+    //    exactly one A22 count (the HASH2 probe counts triangles here)
 #pragma unroll
     for (int e = 0; e < EPT; ++e) {
       const uint32_t x = tid * EPT + e;
       const uint32_t ca = s.cntA[x];
       if (ca) atomicAdd(&S[a0 + x], ca);
+      if (KTG_A22_HASH2) tri_local += ca;
     }
     {
       const uint32_t cp = s.cntP[tid];
