@@ -613,7 +613,8 @@ ktg_status build_working(ktg_engine* e, bool with_sym) {
     return prepare_layout(e, W, true, e->cntw.p, m);
   }
   unsigned long long* sz = e->sym_sizes.p;  // [tot | din | - | inoff | -] x nb
-  k_sym_sizes<<<4 * e->num_sms, 256, 0, s>>>(e->symdeg_w.p, e->cntw.p, n, e->din.p, sz);
+  // (e->sizes is free after the row_ptr scan: it takes the working row ends)
+  k_sym_sizes<<<4 * e->num_sms, 256, 0, s>>>(e->symdeg_w.p, e->cntw.p, n, e->din.p, sz, W.row_ptr.p, e->sizes.p);
   tmp = e->cub_tmp.cap;
   KTG_CUDA(cub::DeviceScan::ExclusiveSum(e->cub_tmp.p, tmp, sz, e->sym_ptr.p, (int)nb, s));
   tmp = e->cub_tmp.cap;
@@ -630,8 +631,7 @@ ktg_status build_working(ktg_engine* e, bool with_sym) {
                                            e->keys_sorted.p, (int64_t)m, 0, (int)B, s));
   mk("bw: in-list sort");
   k_fill_in_all<<<8 * e->num_sms, 256, 0, s>>>(e->vals_sorted.p, e->keys_sorted.p, m, sz + 3 * nb, W.id.p, y,
-                                               e->a22_pe.p, e->a22_pin.p, e->a22_pin_end.p, W.row_ptr.p,
-                                               e->cntw.p);
+                                               e->a22_pe.p, e->a22_pin.p, e->a22_pin_end.p, e->sizes.p);
   KTG_CUDA(cudaGetLastError());
   KTG_CUDA(cudaMemcpyAsync(e->sym_deg.p, e->symdeg_w.p, nb * 4, cudaMemcpyDeviceToDevice, s));
   mk("bw: in-list fill");

@@ -963,10 +963,9 @@ __device__ __forceinline__ uint32_t a22_fbit(uint32_t h) { return (h ^ (h >> 15)
 #ifndef KTG_A22_HASH2
 #define KTG_A22_HASH2 1
 #endif
-#ifndef KTG_A22_FULLSTRIP
-#define KTG_A22_FULLSTRIP 1  // whole strips step without per-element range checks
+#ifndef KTG_A22_UNILOOP
+#define KTG_A22_UNILOOP 1  // step loop with a warp-uniform trip count (lanes past lim carry out-of-range elements)
 #endif
-static_assert(kA22Strip % (2 * 32 * kA22Unroll) == 0, "full and half strips are whole steps");
 #if KTG_A22_HASH2 && !KTG_A22_ASMSMEM
 #error "KTG_A22_HASH2 is implemented on the KTG_A22_ASMSMEM probe path"
 #endif
@@ -1180,19 +1179,20 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ wcost) {
       // run's rk = hh - c * kA22Mul: inside one chunk a value's run end
       // identifies its row (runs are the maximal nonzero stretches). The
       // triangle count comes from the cntA flush.
-      auto probe = [&](uint32_t c, uint32_t slot, uint32_t hh, uint32_t pl) {
-        const uint32_t rk = hh - c * kA22Mul;
-        for (uint32_t h = a22_slot(hh);; h = a22_next(h)) {
-          const uint2 e = lds_v2(sb + oT + (h << 3));
-          if (e.x == 0) break;
-          if (e.x == c && (e.y ^ rk) < 0x10000u) {
-            reds_inc(sb + oA + (e.y & 0xffffu));
-            if (!KTG_A22_LIGHT || (int32_t)pl >= 0) {
-              atomicAdd(&S[slot], 1u);
-              reds_inc(sb + oP + (pl << 2));  // (the flag shifts out)
-            }
-            break;
-          }
+      auto probe = [&](uint32_t c, uint32_t slot, uint32_t hh, uint32_t rk, uint32_t pl) {
+        // the match test first (most filter hits are true at R-MAT rates),
+        // the empty-slot test only on a mismatch
+        uint32_t h = a22_slot(hh);
+        uint2 e = lds_v2(sb + oT + (h << 3));
+        while (!(e.x == c && (e.y ^ rk) < 0x10000u)) {
+          if (e.x == 0) return;
+          h = a22_next(h);
+          e = lds_v2(sb + oT + (h << 3));
+        }
+        reds_inc(sb + oA + (e.y & 0xffffu));
+        if (!KTG_A22_LIGHT || (int32_t)pl >= 0) {
+          atomicAdd(&S[slot], 1u);
+          reds_inc(sb + oP + (pl << 2));  // (the flag shifts out)
         }
       };
 #else
@@ -1294,38 +1294,37 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ wcost) {
 #endif
       // kA22Unroll elements per lane per step, every load issued before any probe
 #if KTG_A22_HASH2
-      // full: every element of the step is inside the strip (no range checks)
-      auto step = [&](const uint32_t f, const bool full) {
+      auto step = [&](const uint32_t f) {
         uint32_t sl[kA22Unroll], ru[kA22Unroll], pv[kA22Unroll], cv[kA22Unroll];
 #pragma unroll
         for (int u = 0; u < kA22Unroll; ++u) {
           const uint32_t fu = f + 32 * u;
-          if (full || fu < lim) advance(fu);
+          if (fu < lim) advance(fu);
           sl[u] = plo + (fu - pb), ru[u] = prun, pv[u] = p;
         }
 #pragma unroll
-        for (int u = 0; u < kA22Unroll; ++u) cv[u] = (full || f + 32 * u < lim) ? col[sl[u]] : 0u;
+        for (int u = 0; u < kA22Unroll; ++u) cv[u] = (f + 32 * u < lim) ? col[sl[u]] : 0u;
         // the kA22Unroll hashes and filter reads as independent chains (the
         // filter bit 31 - (h & 31) lands in the sign: one funnel shift and a
-        // sign test); only the hits branch into the table probe
+        // sign test); only the hits go on to the table probe
 #pragma unroll
         for (int u = 0; u < kA22Unroll; ++u) ru[u] = a22_h2(cv[u], ru[u]);
         bool hit[kA22Unroll];
 #pragma unroll
         for (int u = 0; u < kA22Unroll; ++u) {
           const uint32_t w = lds_u32(sb + oF + ((ru[u] >> 23) << 2));
-          hit[u] = (full || f + 32 * u < lim) && (int32_t)__funnelshift_l(0u, w, ru[u]) < 0;
+          hit[u] = f + 32 * u < lim && (int32_t)__funnelshift_l(0u, w, ru[u]) < 0;
         }
 #pragma unroll
         for (int u = 0; u < kA22Unroll; ++u)
-          if (hit[u]) probe(cv[u], sl[u], ru[u], pv[u]);
+          if (hit[u]) probe(cv[u], sl[u], ru[u], ru[u] - cv[u] * kA22Mul, pv[u]);
+
       };
-#if KTG_A22_FULLSTRIP
-      if (lim - base == strip) {  // a whole strip (strip is a multiple of 32 * kA22Unroll)
-        for (uint32_t f = base + lane; f < lim; f += 32 * kA22Unroll) step(f, true);
-      } else
+#if KTG_A22_UNILOOP
+      for (uint32_t f0 = base; f0 < lim; f0 += 32 * kA22Unroll) step(f0 + lane);  // warp-uniform trip count
+#else
+      for (uint32_t f = base + lane; f < lim; f += 32 * kA22Unroll) step(f);
 #endif
-        for (uint32_t f = base + lane; f < lim; f += 32 * kA22Unroll) step(f, false);
 #else
       for (uint32_t f = base + lane; f < lim; f += 32 * kA22Unroll) {
         uint32_t sl[kA22Unroll], ru[kA22Unroll], pv[kA22Unroll], cv[kA22Unroll];
@@ -2842,7 +2841,8 @@ constexpr int kFillUnroll = KTG_FILL_UNROLL;  // load-time fill passes: entries 
 // rank r, din_w = undirected degree - out-degree; the u64 sizes for the
 // symmetric-row offsets (tot | din) scans.
 __global__ void k_sym_sizes(const uint32_t* __restrict__ symdeg_w, const uint32_t* __restrict__ cntw, uint32_t n,
-                            uint32_t* __restrict__ din_w, unsigned long long* __restrict__ sz) {
+                            uint32_t* __restrict__ din_w, unsigned long long* __restrict__ sz,
+                            const uint32_t* __restrict__ row_ptr_w, uint32_t* __restrict__ rend) {
   const uint32_t nb = n + 2;
   for (uint32_t r = blockIdx.x * blockDim.x + threadIdx.x; r < nb; r += gridDim.x * blockDim.x) {
     const uint32_t tot = (r >= 1 && r <= n) ? symdeg_w[r] : 0u;
@@ -2850,6 +2850,7 @@ __global__ void k_sym_sizes(const uint32_t* __restrict__ symdeg_w, const uint32_
     din_w[r] = tot - dout;
     sz[r] = tot;
     sz[nb + r] = tot - dout;
+    rend[r] = row_ptr_w[r] + dout;  // end of working row r's live part (k_fill_in_all's pin_end)
   }
 }
 
@@ -2921,7 +2922,7 @@ __global__ void k_fill_in_all(const uint32_t* __restrict__ vkeys, const unsigned
                               uint64_t m, const unsigned long long* __restrict__ inoff,
                               const uint32_t* __restrict__ id_w, Sym y, uint32_t* __restrict__ pe,
                               uint2* __restrict__ pin_p, uint32_t* __restrict__ pin_end,
-                              const uint32_t* __restrict__ row_ptr_w, const uint32_t* __restrict__ outdeg_w) {
+                              const uint32_t* __restrict__ rend) {
   const uint64_t stride = (uint64_t)gridDim.x * blockDim.x;
   for (uint64_t i0 = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i0 < m; i0 += kFillUnroll * stride) {
     uint32_t b[kFillUnroll], a[kFillUnroll], slot[kFillUnroll];
@@ -2941,7 +2942,7 @@ __global__ void k_fill_in_all(const uint32_t* __restrict__ vkeys, const unsigned
       if (i < m) {
         id[u] = id_w[slot[u]];
         dst[u] = y.ptr[b[u]] + (i - inoff[b[u]]);
-        end[u] = row_ptr_w[a[u]] + outdeg_w[a[u]];
+        end[u] = rend[a[u]];  // one gather (row_ptr_w + out-degree precombined)
       }
     }
 #pragma unroll
