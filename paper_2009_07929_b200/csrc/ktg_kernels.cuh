@@ -1180,19 +1180,17 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ wcost) {
       // identifies its row (runs are the maximal nonzero stretches). The
       // triangle count comes from the cntA flush.
       auto probe = [&](uint32_t c, uint32_t slot, uint32_t hh, uint32_t rk, uint32_t pl) {
-        // the match test first (most filter hits are true at R-MAT rates),
-        // the empty-slot test only on a mismatch
-        uint32_t h = a22_slot(hh);
-        uint2 e = lds_v2(sb + oT + (h << 3));
-        while (!(e.x == c && (e.y ^ rk) < 0x10000u)) {
-          if (e.x == 0) return;
-          h = a22_next(h);
-          e = lds_v2(sb + oT + (h << 3));
-        }
-        reds_inc(sb + oA + (e.y & 0xffffu));
-        if (!KTG_A22_LIGHT || (int32_t)pl >= 0) {
-          atomicAdd(&S[slot], 1u);
-          reds_inc(sb + oP + (pl << 2));  // (the flag shifts out)
+        for (uint32_t h = a22_slot(hh);; h = a22_next(h)) {
+          const uint2 e = lds_v2(sb + oT + (h << 3));
+          if (e.x == 0) break;
+          if (e.x == c && (e.y ^ rk) < 0x10000u) {
+            reds_inc(sb + oA + (e.y & 0xffffu));
+            if (!KTG_A22_LIGHT || (int32_t)pl >= 0) {
+              atomicAdd(&S[slot], 1u);
+              reds_inc(sb + oP + (pl << 2));  // (the flag shifts out)
+            }
+            break;
+          }
         }
       };
 #else
