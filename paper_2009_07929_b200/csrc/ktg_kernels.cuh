@@ -865,7 +865,7 @@ constexpr int kA22TableBits = 11;          // top hash bits when the table size 
 #endif
 constexpr int kA22Strip = KTG_A22_STRIP;   // flat tail elements a warp takes per grab (at most)
 #ifndef KTG_A22_STRIP_ADAPT
-#define KTG_A22_STRIP_ADAPT 2  // 1: half strips when a batch has < 4 full strips per warp; 2: strips shrink with the remaining work
+#define KTG_A22_STRIP_ADAPT 1  // half strips when a batch has < 4 full strips per warp (balance at the barrier)
 #endif
 constexpr int kA22Table = KTG_A22_TABLE;     // slots (a power of two uses the top hash bits)
 constexpr int kA22Unroll = KTG_A22_UNROLL;     // tail elements per lane per step (loads in flight)
@@ -1155,23 +1155,9 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ wcost) {
     uint32_t tri_task = 0;
     for (;;) {
       uint32_t base = 0;
-#if KTG_A22_STRIP_ADAPT == 2
-      // strips shrink (256 -> 32 elements) as the task's remaining work
-      // drops below two strips per warp, so the 8 warps reach the task's
-      // barrier together (a peek at the counter; the atomic decides)
-      uint32_t strip = kA22Strip;
-      if (lane == 0) {
-        const uint32_t nx = *(volatile uint32_t*)&s.next;
-        const uint32_t rem = nx < W ? W - nx : 0u;
-        while (strip > 32u && strip * (2u * NW) > rem) strip >>= 1;
-        base = atomicAdd(&s.next, strip);
-      }
-      strip = __shfl_sync(0xffffffffu, strip, 0);
-#else
       // (short batches: half strips, so the 8 warps reach the barrier together)
       const uint32_t strip = (KTG_A22_STRIP_ADAPT && W < 4u * NW * kA22Strip) ? kA22Strip / 2 : kA22Strip;
       if (lane == 0) base = atomicAdd(&s.next, strip);
-#endif
       base = __shfl_sync(0xffffffffu, base, 0);
       if (base >= W) break;
       const uint32_t lim = min(base + strip, W);
