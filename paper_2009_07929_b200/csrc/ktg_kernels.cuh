@@ -861,11 +861,11 @@ constexpr int kA22Batch = 256;
 #endif
 constexpr int kA22TableBits = 11;          // top hash bits when the table size is a power of two
 #ifndef KTG_A22_STRIP
-#define KTG_A22_STRIP 256
+#define KTG_A22_STRIP 512
 #endif
 constexpr int kA22Strip = KTG_A22_STRIP;   // flat tail elements a warp takes per grab (at most)
 #ifndef KTG_A22_STRIP_ADAPT
-#define KTG_A22_STRIP_ADAPT 1  // half strips when a batch has < 4 full strips per warp (balance at the barrier)
+#define KTG_A22_STRIP_ADAPT 1  // strips halve (down to 128) while a batch has < 4 per warp (balance at the barrier)
 #endif
 constexpr int kA22Table = KTG_A22_TABLE;     // slots (a power of two uses the top hash bits)
 constexpr int kA22Unroll = KTG_A22_UNROLL;     // tail elements per lane per step (loads in flight)
@@ -1156,7 +1156,10 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ wcost) {
     for (;;) {
       uint32_t base = 0;
       // (short batches: half strips, so the 8 warps reach the barrier together)
-      const uint32_t strip = (KTG_A22_STRIP_ADAPT && W < 4u * NW * kA22Strip) ? kA22Strip / 2 : kA22Strip;
+      // (big batches: 512-element strips, fewer grabs and pivot searches)
+      uint32_t strip = kA22Strip;
+      if (KTG_A22_STRIP_ADAPT)
+        while (strip > 128u && W < 4u * NW * strip) strip >>= 1;
       if (lane == 0) base = atomicAdd(&s.next, strip);
       base = __shfl_sync(0xffffffffu, base, 0);
       if (base >= W) break;
