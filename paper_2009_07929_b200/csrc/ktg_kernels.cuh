@@ -492,38 +492,6 @@ __device__ __forceinline__ uint32_t lb_global(const uint32_t* __restrict__ a, ui
 }
 
 
-// Both lower bounds of k1 <= k2 in the sorted a[lo, hi), by interleaved
-// 4-ary searches: three independent loads per key per round (log4 rounds of
-// dependent latency instead of log2, and the two keys overlap) -- the
-// per-pivot tail clipping of k_support_a22, where every thread of the CTA
-// waits at the scan barrier for the slowest pivot's search chain.
-__device__ __forceinline__ void lb2_global(const uint32_t* __restrict__ a, uint32_t lo, uint32_t hi, uint32_t k1,
-                                           uint32_t k2, uint32_t* r1, uint32_t* r2) {
-  // answer_i in [lo_i, hi_i]: a[hi_i] >= k_i, or hi_i is the range end
-  uint32_t lo1 = lo, hi1 = hi, lo2 = lo, hi2 = hi;
-  while (hi1 - lo1 > 3u || hi2 - lo2 > 3u) {
-    const uint32_t q1 = (hi1 - lo1) >> 2, q2 = (hi2 - lo2) >> 2;
-    uint32_t v1 = 0, v2 = 0, v3 = 0, w1 = 0, w2 = 0, w3 = 0;
-    if (q1) v1 = __ldg(a + lo1 + q1), v2 = __ldg(a + lo1 + 2 * q1), v3 = __ldg(a + lo1 + 3 * q1);
-    if (q2) w1 = __ldg(a + lo2 + q2), w2 = __ldg(a + lo2 + 2 * q2), w3 = __ldg(a + lo2 + 3 * q2);
-    if (q1) {
-      if (v3 < k1) lo1 += 3 * q1 + 1;
-      else if (v2 < k1) hi1 = lo1 + 3 * q1, lo1 += 2 * q1 + 1;
-      else if (v1 < k1) hi1 = lo1 + 2 * q1, lo1 += q1 + 1;
-      else hi1 = lo1 + q1;
-    }
-    if (q2) {
-      if (w3 < k2) lo2 += 3 * q2 + 1;
-      else if (w2 < k2) hi2 = lo2 + 3 * q2, lo2 += 2 * q2 + 1;
-      else if (w1 < k2) hi2 = lo2 + 2 * q2, lo2 += q2 + 1;
-      else hi2 = lo2 + q2;
-    }
-  }
-  while (lo1 < hi1 && __ldg(a + lo1) < k1) ++lo1;
-  while (lo2 < hi2 && __ldg(a + lo2) < k2) ++lo2;
-  *r1 = lo1, *r2 = lo2;
-}
-
 // Block-wide exclusive scan of one u32 per thread; returns the prefix, total
 // in *total. Uses red as scratch.
 __device__ __forceinline__ uint32_t block_exscan(uint32_t v, uint32_t* red, uint32_t* total) {
@@ -998,9 +966,6 @@ __device__ __forceinline__ uint32_t a22_fbit(uint32_t h) { return (h ^ (h >> 15)
 #ifndef KTG_A22_HASH2
 #define KTG_A22_HASH2 1
 #endif
-#ifndef KTG_A22_LB4
-#define KTG_A22_LB4 1  // tail clipping by interleaved 4-ary searches
-#endif
 #ifndef KTG_A22_UNILOOP
 #define KTG_A22_UNILOOP 1  // step loop with a warp-uniform trip count (lanes past lim carry out-of-range elements)
 #endif
@@ -1108,12 +1073,8 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ wcost) {
         uint32_t tlo = ps + 1, thi = iend;
         const uint32_t tb = (run >> 16) & 0x3fffu, te = run & 0xffffu;
         if (run & 0x40000000u) {  // partial run: clip the tail
-#if KTG_A22_LB4
-          lb2_global(col, tlo, thi, col[a0 + tb], col[a0 + te - 1] + 1, &tlo, &thi);
-#else
           tlo = lb_global(col, tlo, thi, col[a0 + tb]);
           thi = lb_global(col, tlo, thi, col[a0 + te - 1] + 1);
-#endif
         }
         if (thi > tlo) {
           cost = thi - tlo;
