@@ -967,7 +967,7 @@ __device__ __forceinline__ uint32_t a22_fbit(uint32_t h) { return (h ^ (h >> 15)
 #define KTG_A22_HASH2 1
 #endif
 #ifndef KTG_A22_EARLYCLAIM
-#define KTG_A22_EARLYCLAIM 1  // the next task is claimed under the flush barrier (one barrier fewer per task)
+#define KTG_A22_EARLYCLAIM 0  // 1: the next task is claimed under the flush barrier (one barrier fewer per task)
 #endif
 #ifndef KTG_A22_UNILOOP
 #define KTG_A22_UNILOOP 1  // step loop with a warp-uniform trip count (lanes past lim carry out-of-range elements)
