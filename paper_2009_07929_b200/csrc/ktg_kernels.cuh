@@ -966,9 +966,6 @@ __device__ __forceinline__ uint32_t a22_fbit(uint32_t h) { return (h ^ (h >> 15)
 #ifndef KTG_A22_HASH2
 #define KTG_A22_HASH2 1
 #endif
-#ifndef KTG_A22_EARLYCLAIM
-#define KTG_A22_EARLYCLAIM 0  // 1: the next task is claimed under the flush barrier (one barrier fewer per task)
-#endif
 #ifndef KTG_A22_UNILOOP
 #define KTG_A22_UNILOOP 1  // step loop with a warp-uniform trip count (lanes past lim carry out-of-range elements)
 #endif
@@ -1011,23 +1008,10 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ wcost) {
     s.task = tt < (part ? g.a22_hi : a.ntasks) ? tt : 0xffffffffu;
     s.next = 0;
   };
-#if KTG_A22_EARLYCLAIM
-  // a task that reached the flush claims the next one there: s.task / s.next
-  // are dead after the strips, so the flush barrier doubles as the claim's
-  bool claimed = false;
-#endif
 
   for (;;) {
-#if KTG_A22_EARLYCLAIM
-    if (!claimed) {
-      if (tid == 0) claim();
-      __syncthreads();
-    }
-    claimed = false;
-#else
     if (tid == 0) claim();
     __syncthreads();
-#endif
     const uint32_t t = s.task;
     if (t == 0xffffffffu) break;
     const uint2 tk = a.tasks[a.ntasks - 1 - t];  // dense (high-rank) chunks first
@@ -1379,10 +1363,6 @@ k_support_a22(Graph g, Sym y, A22 a, unsigned long long* __restrict__ wcost) {
       const uint32_t cp = s.cntP[tid];
       if (cp) atomicAdd(&S[s.ps[tid]], cp);
     }
-#if KTG_A22_EARLYCLAIM
-    if (tid == 0) claim();
-    claimed = true;
-#endif
     __syncthreads();
   }
 #pragma unroll
